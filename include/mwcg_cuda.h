@@ -1,0 +1,157 @@
+/*
+ * mwcg_cuda.h -- C ABI of libmwcg_cuda.so, the B200 (sm_100a) multi-word CG.
+ *
+ * This is the drop-in boundary for the reference package `mwcg`
+ * (/root/reference/pkg/src/mwcg).  The reference has no FFI of its own: its
+ * only native boundary is the Python -> numba call of the operator table
+ * `_fast.KERNELS[mode][op]` (_fast.py:592-633, dispatched from
+ * kernels.py:174-296) plus the solver entry `cg_solve` (cg.py:78-183).  Each
+ * entry point below names the reference interface it replaces.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only; no torch types.  Vector arguments are
+ *    DEVICE pointers to structure-of-arrays word planes: word k of element i
+ *    at v[k*ld + i] (the reference stores AoS records, kernels.py:39-40, 69-74;
+ *    the values per word are identical).
+ *  - mode: 0 fp64, 1 dw, 2 qdw, 3 tw, 4 qtw (kernels.py:35 MODES order).
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream).  Every call
+ *    is stream-ordered; only the *_state / *_metrics / mwcg_cg_solve calls
+ *    synchronize.
+ *  - Return value 0 = success; otherwise a cudaError_t (< 1000) or
+ *    MWCG_ERR_VALUE (1001, the reference's ValueError cases) /
+ *    MWCG_ERR_STATE (1002).  mwcg_last_error() gives the message
+ *    (thread-local).
+ *  - There is no CPU fallback: without a CUDA device every compute entry
+ *    point returns a cudaError_t.
+ */
+#ifndef MWCG_CUDA_H
+#define MWCG_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MWCG_ABI_VERSION 1
+
+enum { MWCG_FP64 = 0, MWCG_DW = 1, MWCG_QDW = 2, MWCG_TW = 3, MWCG_QTW = 4 };
+/* Normalization (cg.py:27-32) */
+enum { MWCG_NORM_NONE = 0, MWCG_NORM_AFTER_AXPY = 1, MWCG_NORM_EVERY_OP = 2 };
+/* Dot-product reduction shape: the canonical device tile tree (fast), or
+ * the reference's P-partition sequential shape (bitwise equal to the
+ * reference's cg_solve(partitions=P); kernels.py:158-162, _fast.py:342-356). */
+enum { MWCG_RED_TILE = 0, MWCG_RED_PARTITIONS = 1 };
+/* SolverResult.reason (cg.py:69) */
+enum { MWCG_RUNNING = 0, MWCG_CONVERGED = 1, MWCG_MAX_ITERATIONS = 2, MWCG_BREAKDOWN = 3 };
+
+typedef struct mwcg_matrix mwcg_matrix;
+typedef struct mwcg_solver mwcg_solver;
+
+/* SolverConfig (cg.py:35-55) minus the per-solve scalars */
+typedef struct {
+    int mode;
+    int normalization;
+    int reduction;
+    int reserved;
+    int64_t partitions;
+} mwcg_solver_config;
+
+typedef struct {
+    int64_t k;           /* completed iterations */
+    int64_t iterations;  /* SolverResult.iterations once stopped */
+    int status;          /* MWCG_RUNNING / CONVERGED / MAX_ITERATIONS / BREAKDOWN */
+    int reserved;
+    double rel;          /* recurrence residual ||r||/||b||, FP64 collapse */
+    double rho[3], alpha[3], beta[3];
+} mwcg_state;
+
+typedef struct {
+    int64_t iterations;
+    int64_t n_hist;
+    int status;
+    int reserved;
+    double final_rel;
+    double loop_ms;      /* device time of the iteration loop (CUDA events) */
+    double history_ms;   /* device time spent in history metrics */
+    double stage_ms[3];  /* profile=1 only: K1 spmv+p.q, K2 update+r.r, K3 xpay */
+} mwcg_solve_result;
+
+/* ---- library ---- */
+int mwcg_abi_version(void);
+const char *mwcg_last_error(void);
+int mwcg_words(int mode);                         /* kernels.py:43-46 mode_words */
+int mwcg_device_check(void);                      /* 0 if an sm_100 device is usable */
+
+/* ---- matrix: CsrMatrix (sparse.py:36-87) -> device SELL-32 ----
+ * row_ptr/col_idx: device pointers, int64 (index_bytes=8, the reference's
+ * dtype, sparse.py:47-48) or int32 (index_bytes=4). values: device f64. */
+int mwcg_matrix_create(mwcg_matrix **out, int64_t n_rows, int64_t n_cols, int64_t nnz,
+                       const void *row_ptr, const void *col_idx, const double *values,
+                       int index_bytes, void *stream);
+int mwcg_matrix_destroy(mwcg_matrix *A);
+int mwcg_matrix_info(const mwcg_matrix *A, int64_t *n_rows, int64_t *n_cols, int64_t *nnz,
+                     int64_t *padded_entries);
+
+/* ---- operator table: replaces _fast.KERNELS[mode][op] (_fast.py:592-633) ---- */
+/* spmv_<mode> (_fast.py:284-290, 329-339, 383-393, 443-455, 501-513) */
+int mwcg_spmv(int mode, const mwcg_matrix *A, const double *x, int64_t ldx, double *y,
+              int64_t ldy, void *stream);
+/* dot_<mode> (_fast.py:293-304, 342-356, 396-410, 458-474, 516-532).
+ * partitions >= 1: the reference shape; partitions == 0: the device tile
+ * tree.  out: device, 3 doubles.  work: device scratch of
+ * mwcg_dot_work_bytes() bytes, ZERO-initialised before first use. */
+int64_t mwcg_dot_work_bytes(int64_t n, int64_t partitions);
+int mwcg_dot(int mode, int64_t n, const double *x, int64_t ldx, const double *y, int64_t ldy,
+             int64_t partitions, double *out, void *work, void *stream);
+/* axpy_<mode> (_fast.py:307-310, 359-363, 413-417, 477-481, 535-539);
+ * alpha: HOST pointer to w words */
+int mwcg_axpy(int mode, int64_t n, const double *alpha, const double *x, int64_t ldx, double *y,
+              int64_t ldy, void *stream);
+/* scal_add_<mode> (_fast.py:313-316, 366-370, ...): p <- r + beta p */
+int mwcg_scal_add(int mode, int64_t n, const double *beta, double *p, int64_t ldp,
+                  const double *r, int64_t ldr, void *stream);
+/* residual_<mode> (_fast.py:319-322, ...): r = b - q, b FP64 */
+int mwcg_residual(int mode, int64_t n, const double *b, const double *q, int64_t ldq, double *r,
+                  int64_t ldr, void *stream);
+/* normalize_arr_q{dw,tw} (_fast.py:433-436, 555-558); no-op for other modes */
+int mwcg_normalize(int mode, int64_t n, double *v, int64_t ld, void *stream);
+/* scalar ops on device pointers (3 doubles each), codes:
+ * 0 add 1 mul 2 dxmul 3 dxadd 4 normalize 5 div 6 neg 7 two_sum
+ * 8 quick_two_sum 9 two_prod 10 collapse (multiword.py / eft.py) */
+int mwcg_scalar_op(int op, int mode, const double *a, const double *b, double *out, void *stream);
+/* norm2_fp64 (kernels.py:290-296, sumsq_collapsed_1 _fast.py:565-571):
+ * sequential unfused sum of squares of a HOST vector, then sqrt. */
+int mwcg_norm2_host(const double *b, int64_t n, double *out);
+
+/* ---- solver: replaces cg_solve (cg.py:78-183) ---- */
+/* x: device buffer of w*n doubles for the solution words (NULL: internal) */
+int mwcg_solver_create(mwcg_solver **out, const mwcg_matrix *A, const mwcg_solver_config *cfg,
+                       double *x, void *stream);
+int mwcg_solver_destroy(mwcg_solver *s);
+/* b, x0 (nullable, FP64 initial guess), x_star (nullable): device f64[n].
+ * b_norm: norm2_fp64(b) (0 is replaced by 1, cg.py:121-123). */
+int mwcg_solver_start(mwcg_solver *s, const double *b, double b_norm, const double *x0,
+                      const double *x_star, double epsilon, int64_t max_iterations);
+/* enqueue iterations until stop or k == k_stop (one graph launch) */
+int mwcg_solver_run(mwcg_solver *s, int64_t k_stop);
+/* same, kernel-by-kernel with CUDA events; ms[0..2] += per-stage device ms */
+int mwcg_solver_run_profiled(mwcg_solver *s, int64_t k_stop, double *ms);
+int mwcg_solver_state(mwcg_solver *s, mwcg_state *out);
+/* norm_metrics_tw (kernels.py:305-328) of the current iterate */
+int mwcg_solver_metrics(mwcg_solver *s, double *err, double *true_res);
+/* whole solve with history (ConvergenceRecord, cg.py:58-63, 129-136) */
+int mwcg_cg_solve(mwcg_solver *s, const double *b, double b_norm, const double *x0,
+                  const double *x_star, double epsilon, int64_t max_iterations,
+                  int64_t history_stride, int profile, mwcg_solve_result *res,
+                  int64_t hist_cap, int64_t *h_k, double *h_rel, double *h_true, double *h_err);
+
+/* ---- measurement helpers (bench.py) ---- */
+/* FP64 pipe microbenchmark: DFMA chains on all SMs; returns FP64 ops/s
+ * (FMA = 1 op, the SURVEY §8(d) convention) and the elapsed ms. */
+int mwcg_fp64_peak(double *ops_per_s, double *ms, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MWCG_CUDA_H */

@@ -1,0 +1,887 @@
+// cg.cu -- the fused CG iteration (Algorithm 1, cg.py:78-183) on device.
+//
+// One iteration = three kernels, captured once into a CUDA graph whose body
+// sits inside a conditional WHILE node, so a whole segment of iterations runs
+// with no host round-trip:
+//
+//   K1 cg_spmv_pq   q = A p (SELL-32, per-row left-to-right), [every-op: norm q],
+//                   p.q tile partials; the last CTA reduces them in the
+//                   canonical order and runs the scalar step
+//                   (pq breakdown test cg.py:156-158, alpha = rho/pq cg.py:159).
+//   K2 cg_update    x += alpha p [norm x], r += (-alpha) q [norm r], r.r tile
+//                   partials; last CTA: rho_new, rel (cg.py:167-169), stop /
+//                   breakdown tests (cg.py:172-176), beta (cg.py:177), k++,
+//                   and the WHILE condition.
+//   K3 cg_xpay      p = r + beta p [norm p]   (cg.py:178-180)
+//
+// Reference-order mode (reduction=partitions, bitwise equal to the reference
+// cg_solve(partitions=P)) replaces the fused tile-tree dots by the reference's
+// P-partition sequential dots (two extra kernels per dot).
+#include <cmath>
+#include <vector>
+#include "ops.cuh"
+#include "mwcg_internal.h"
+#include "../../include/mwcg_cuda.h"
+
+namespace mwcg {
+
+using namespace mw;
+
+__device__ __forceinline__ void set_cond(cudaGraphConditionalHandle h, int use_cond, unsigned v) {
+    if (use_cond) cudaGraphSetConditional(h, v);
+}
+
+// ---------------------------------------------------------------- scalar steps
+template <int M>
+__device__ void scalar_alpha(CgState *st, V<Arith<M>::W> pq, cudaGraphConditionalHandle h, int use_cond) {
+    using Ar = Arith<M>;
+    constexpr int W = Ar::W;
+    for (int k = 0; k < W; k++) st->pq[k] = pq.w[k];
+    double pq_f = Ar::collapse(pq);
+    if (pq_f == 0.0 || !isfinite(pq_f)) {
+        st->status = BREAKDOWN;
+        st->iterations = st->k;  // finish(False, "breakdown", k - 1): cg.py:157-158
+        set_cond(h, use_cond, 0u);
+        return;
+    }
+    V<W> rho;
+    for (int k = 0; k < W; k++) rho.w[k] = st->rho[k];
+    V<W> a = Ar::div(rho, pq);
+    for (int k = 0; k < W; k++) {
+        st->alpha[k] = a.w[k];
+        st->neg_alpha[k] = -a.w[k];
+    }
+}
+
+template <int M>
+__device__ void scalar_beta(CgState *st, V<Arith<M>::W> rho_new, cudaGraphConditionalHandle h,
+                            int use_cond) {
+    using Ar = Arith<M>;
+    constexpr int W = Ar::W;
+    long long k = st->k + 1;
+    st->k = k;
+    for (int i = 0; i < W; i++) st->rho_new[i] = rho_new.w[i];
+    double rf = Ar::collapse(rho_new);
+    double rel = sqrt(fabs(rf)) / st->b_norm;  // rel_residual: cg.py:125-127
+    st->rel = rel;
+    if (rel < st->eps) {
+        st->status = CONVERGED;
+        st->iterations = k;
+    } else if (rf == 0.0 || !isfinite(rf)) {
+        st->status = BREAKDOWN;
+        st->iterations = k;
+    } else {
+        V<W> rho;
+        for (int i = 0; i < W; i++) rho.w[i] = st->rho[i];
+        V<W> b = Ar::div(rho_new, rho);
+        for (int i = 0; i < W; i++) {
+            st->beta[i] = b.w[i];
+            st->rho[i] = rho_new.w[i];
+        }
+        if (k >= st->max_iters) {
+            st->status = MAX_ITERS;
+            st->iterations = k;
+        }
+    }
+    set_cond(h, use_cond, (st->status == RUNNING && k < st->k_stop) ? 1u : 0u);
+}
+
+template <int M>
+__device__ void scalar_init(CgState *st, V<Arith<M>::W> rho) {
+    using Ar = Arith<M>;
+    constexpr int W = Ar::W;
+    for (int i = 0; i < W; i++) st->rho[i] = rho.w[i];
+    double rel = sqrt(fabs(Ar::collapse(rho))) / st->b_norm;
+    st->rel = rel;
+    st->k = 0;
+    if (rel < st->eps) {  // cg.py:147-148
+        st->status = CONVERGED;
+        st->iterations = 0;
+    } else if (st->max_iters <= 0) {
+        st->status = MAX_ITERS;
+        st->iterations = 0;
+    } else {
+        st->status = RUNNING;
+    }
+}
+
+__device__ __forceinline__ bool stopped(const CgState *st, cudaGraphConditionalHandle h, int use_cond) {
+    if (st->status != RUNNING) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) set_cond(h, use_cond, 0u);
+        return true;
+    }
+    return false;
+}
+
+// ---------------------------------------------------------------- K1
+template <int M, bool FUSED>
+__global__ void __launch_bounds__(TILE_THREADS)
+    cg_spmv_pq(SellMatrix A, const double *__restrict__ p, double *__restrict__ q, int64_t ld,
+               double *__restrict__ part, int64_t ntiles, CgState *st, cudaGraphConditionalHandle h,
+               int use_cond) {
+    using Ar = Arith<M>;
+    constexpr int W = Ar::W;
+    __shared__ double smem[W * TILE_THREADS / 32];
+    __shared__ int s_last;
+    if (stopped(st, h, use_cond)) return;
+    const bool norm_all = st->norm_all != 0;
+    const int64_t n = A.n_rows;
+    const int64_t base = (int64_t)blockIdx.x * TILE + threadIdx.x;
+    V<W> acc = zero<W>();
+#pragma unroll 1
+    for (int j = 0; j < TILE_ELEMS; j++) {
+        int64_t row = base + j * TILE_THREADS;
+        if (row < n) {
+            V<W> s = spmv_row<M>(A, p, ld, row);
+            if (norm_all) s = Ar::norm(s);
+            store<W>(q, ld, row, s);
+            if (FUSED) acc = Ar::add(acc, Ar::mul(load_ro<W>(p, ld, row), s));
+        }
+    }
+    if (!FUSED) return;
+    acc = block_tree<M, TILE_THREADS>(acc, smem);
+    if (threadIdx.x == 0) store<W>(part, ntiles, blockIdx.x, acc);
+    if (!last_block_done(&st->ticket[0], &s_last)) return;
+    V<W> pq = reduce_partials_block<M>(part, ntiles, ntiles, smem);
+    if (threadIdx.x == 0) {
+        st->ticket[0] = 0u;
+        scalar_alpha<M>(st, pq, h, use_cond);
+    }
+}
+
+// ---------------------------------------------------------------- K2
+template <int M, bool FUSED>
+__global__ void __launch_bounds__(TILE_THREADS)
+    cg_update(int64_t n, double *__restrict__ x, double *__restrict__ r, const double *__restrict__ p,
+              const double *__restrict__ q, int64_t ld, double *__restrict__ part, int64_t ntiles,
+              CgState *st, cudaGraphConditionalHandle h, int use_cond) {
+    using Ar = Arith<M>;
+    constexpr int W = Ar::W;
+    __shared__ double smem[W * TILE_THREADS / 32];
+    __shared__ int s_last;
+    if (stopped(st, h, use_cond)) return;
+    const bool norm_all = st->norm_all != 0, norm_r = st->norm_r != 0;
+    V<W> alpha, nalpha;
+#pragma unroll
+    for (int k = 0; k < W; k++) {
+        alpha.w[k] = st->alpha[k];
+        nalpha.w[k] = st->neg_alpha[k];
+    }
+    const int64_t base = (int64_t)blockIdx.x * TILE + threadIdx.x;
+    V<W> acc = zero<W>();
+#pragma unroll
+    for (int j = 0; j < TILE_ELEMS; j++) {
+        int64_t i = base + j * TILE_THREADS;
+        if (i < n) {
+            V<W> xi = Ar::add(load<W>(x, ld, i), Ar::mul(alpha, load_ro<W>(p, ld, i)));
+            if (norm_all) xi = Ar::norm(xi);
+            store<W>(x, ld, i, xi);
+            V<W> ri = Ar::add(load<W>(r, ld, i), Ar::mul(nalpha, load_ro<W>(q, ld, i)));
+            if (norm_r) ri = Ar::norm(ri);
+            store<W>(r, ld, i, ri);
+            if (FUSED) acc = Ar::add(acc, Ar::mul(ri, ri));
+        }
+    }
+    if (!FUSED) return;
+    acc = block_tree<M, TILE_THREADS>(acc, smem);
+    if (threadIdx.x == 0) store<W>(part, ntiles, blockIdx.x, acc);
+    if (!last_block_done(&st->ticket[1], &s_last)) return;
+    V<W> rn = reduce_partials_block<M>(part, ntiles, ntiles, smem);
+    if (threadIdx.x == 0) {
+        st->ticket[1] = 0u;
+        scalar_beta<M>(st, rn, h, use_cond);
+    }
+}
+
+// ---------------------------------------------------------------- K3
+template <int M>
+__global__ void __launch_bounds__(TILE_THREADS)
+    cg_xpay(int64_t n, double *__restrict__ p, const double *__restrict__ r, int64_t ld, CgState *st,
+            cudaGraphConditionalHandle h, int use_cond) {
+    using Ar = Arith<M>;
+    constexpr int W = Ar::W;
+    if (stopped(st, h, use_cond)) return;
+    const bool norm_all = st->norm_all != 0;
+    V<W> beta;
+#pragma unroll
+    for (int k = 0; k < W; k++) beta.w[k] = st->beta[k];
+    const int64_t base = (int64_t)blockIdx.x * TILE + threadIdx.x;
+#pragma unroll
+    for (int j = 0; j < TILE_ELEMS; j++) {
+        int64_t i = base + j * TILE_THREADS;
+        if (i < n) {
+            V<W> pi = Ar::add(load_ro<W>(r, ld, i), Ar::mul(beta, load<W>(p, ld, i)));
+            if (norm_all) pi = Ar::norm(pi);
+            store<W>(p, ld, i, pi);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- init
+// r = b - q (residual, cg.py:114), [norm r] (cg.py:115-116), p = r (117),
+// rho = r.r (118), rel, converged-at-0 test (147-148).
+template <int M, bool FUSED>
+__global__ void __launch_bounds__(TILE_THREADS)
+    cg_init(int64_t n, const double *__restrict__ b, const double *__restrict__ q, double *__restrict__ r,
+            double *__restrict__ p, int64_t ld, double *__restrict__ part, int64_t ntiles, CgState *st) {
+    using Ar = Arith<M>;
+    constexpr int W = Ar::W;
+    __shared__ double smem[W * TILE_THREADS / 32];
+    __shared__ int s_last;
+    const bool norm_r = st->norm_r != 0;
+    const int64_t base = (int64_t)blockIdx.x * TILE + threadIdx.x;
+    V<W> acc = zero<W>();
+#pragma unroll
+    for (int j = 0; j < TILE_ELEMS; j++) {
+        int64_t i = base + j * TILE_THREADS;
+        if (i < n) {
+            V<W> ri = Ar::dxadd(b[i], neg<W>(load<W>(q, ld, i)));
+            if (norm_r) ri = Ar::norm(ri);
+            store<W>(r, ld, i, ri);
+            store<W>(p, ld, i, ri);
+            if (FUSED) acc = Ar::add(acc, Ar::mul(ri, ri));
+        }
+    }
+    if (!FUSED) return;
+    acc = block_tree<M, TILE_THREADS>(acc, smem);
+    if (threadIdx.x == 0) store<W>(part, ntiles, blockIdx.x, acc);
+    if (!last_block_done(&st->ticket[2], &s_last)) return;
+    V<W> rho = reduce_partials_block<M>(part, ntiles, ntiles, smem);
+    if (threadIdx.x == 0) {
+        st->ticket[2] = 0u;
+        scalar_init<M>(st, rho);
+    }
+}
+
+// ---------------------------------------------------------------- reference-order dots
+template <int M>
+__global__ void cg_dot_part(int64_t n, const double *__restrict__ x, const double *__restrict__ y,
+                            int64_t ld, int64_t parts, double *__restrict__ part, const CgState *st,
+                            int check_status) {
+    using Ar = Arith<M>;
+    constexpr int W = Ar::W;
+    if (check_status && st->status != RUNNING) return;
+    int64_t pidx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (pidx >= parts) return;
+    int64_t lo = (int64_t)(((__int128)n * pidx) / parts);
+    int64_t hi = (int64_t)(((__int128)n * (pidx + 1)) / parts);
+    V<W> t = zero<W>();
+    for (int64_t i = lo; i < hi; i++) t = Ar::add(t, Ar::mul(load<W>(x, ld, i), load<W>(y, ld, i)));
+    store<W>(part, parts, pidx, t);
+}
+
+// phase 0: init (rho), 1: alpha (pq), 2: beta (rho_new)
+template <int M>
+__global__ void cg_ref_combine(const double *__restrict__ part, int64_t parts, CgState *st, int phase,
+                               cudaGraphConditionalHandle h, int use_cond) {
+    using Ar = Arith<M>;
+    constexpr int W = Ar::W;
+    if (phase != 0 && st->status != RUNNING) {
+        set_cond(h, use_cond, 0u);
+        return;
+    }
+    V<W> s = load<W>(part, parts, 0);
+    for (int64_t pi = 1; pi < parts; pi++) s = Ar::add(s, load<W>(part, parts, pi));
+    if (phase == 0) scalar_init<M>(st, s);
+    else if (phase == 1) scalar_alpha<M>(st, s, h, use_cond);
+    else scalar_beta<M>(st, s, h, use_cond);
+}
+
+// ---------------------------------------------------------------- history metrics
+// norm_metrics_tw (kernels.py:305-328): x promoted to TW (107-112), TW SpMV,
+// TW residual b - Ax, and x* - x; the TW sums of squares use the solver's
+// reduction shape (tile tree, or partitions=1 in reference-order mode,
+// matching _tw_norm_sq kernels.py:299-302).
+template <int M>
+__global__ void promote_kernel(int64_t n, const double *__restrict__ x, int64_t ldx,
+                               double *__restrict__ xt) {
+    constexpr int W = Arith<M>::W;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+        for (int k = 0; k < 3; k++) xt[k * n + i] = k < W ? x[k * ldx + i] : 0.0;
+    }
+}
+
+__global__ void promote_fp64_kernel(int64_t n, const double *__restrict__ v, double *__restrict__ vt) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        vt[i] = v[i];
+        vt[n + i] = 0.0;
+        vt[2 * n + i] = 0.0;
+    }
+}
+
+__global__ void __launch_bounds__(TILE_THREADS)
+    metrics_vec_kernel(SellMatrix A, const double *__restrict__ xt, const double *__restrict__ b,
+                       const double *__restrict__ xs, double *__restrict__ res, double *__restrict__ diff) {
+    const int64_t n = A.n_rows;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        V<3> qi = spmv_row<TW>(A, xt, n, i);
+        store<3>(res, n, i, dxtw_add(b[i], neg<3>(qi)));
+        if (xs) store<3>(diff, n, i, dxtw_add(xs[i], neg<3>(load<3>(xt, n, i))));
+    }
+}
+
+}  // namespace mwcg
+
+// =====================================================================
+// Host runtime
+// =====================================================================
+using namespace mwcg;
+
+struct mwcg_matrix {
+    SellMatrixOwned *M;
+};
+
+struct mwcg_solver {
+    SellMatrix A{};
+    int mode = 0, W = 1;
+    mwcg_solver_config cfg{};
+    int64_t n = 0, ntiles = 0, parts = 1;
+    bool fused = true;
+    cudaStream_t stream = nullptr;       // caller's stream (all work ordered on it)
+    cudaStream_t cap = nullptr;          // private stream for graph capture
+    double *x = nullptr, *r = nullptr, *p = nullptr, *q = nullptr;
+    bool own_x = false;
+    double *part = nullptr;
+    CgState *st = nullptr;
+    CgState *st_host = nullptr;          // pinned mirror
+    long long *kstop_host = nullptr;     // pinned
+    const double *b = nullptr, *x_star = nullptr;
+    // metrics scratch
+    double *xt = nullptr, *res = nullptr, *diff = nullptr, *bt = nullptr;
+    double *mpart = nullptr, *mout = nullptr, *mout_host = nullptr;
+    unsigned int *mticket = nullptr;
+    double bnorm_sq = 1.0, xs_sq = 1.0;
+    bool norms_ready = false;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cudaGraphConditionalHandle cond{};
+    cudaEvent_t ev[8] = {};
+};
+
+namespace {
+
+template <int M>
+int enqueue_iteration(mwcg_solver *s, cudaStream_t st, cudaGraphConditionalHandle h, int use_cond) {
+    const unsigned tiles = (unsigned)s->ntiles;
+    const int64_t ld = s->n;
+    if (s->fused) {
+        cg_spmv_pq<M, true><<<tiles, TILE_THREADS, 0, st>>>(s->A, s->p, s->q, ld, s->part, s->ntiles,
+                                                             s->st, h, use_cond);
+        cg_update<M, true><<<tiles, TILE_THREADS, 0, st>>>(s->n, s->x, s->r, s->p, s->q, ld, s->part,
+                                                            s->ntiles, s->st, h, use_cond);
+    } else {
+        const unsigned pb = (unsigned)((s->parts + 127) / 128);
+        cg_spmv_pq<M, false><<<tiles, TILE_THREADS, 0, st>>>(s->A, s->p, s->q, ld, s->part, s->ntiles,
+                                                              s->st, h, use_cond);
+        cg_dot_part<M><<<pb, 128, 0, st>>>(s->n, s->p, s->q, ld, s->parts, s->part, s->st, 1);
+        cg_ref_combine<M><<<1, 1, 0, st>>>(s->part, s->parts, s->st, 1, h, use_cond);
+        cg_update<M, false><<<tiles, TILE_THREADS, 0, st>>>(s->n, s->x, s->r, s->p, s->q, ld, s->part,
+                                                             s->ntiles, s->st, h, use_cond);
+        cg_dot_part<M><<<pb, 128, 0, st>>>(s->n, s->r, s->r, ld, s->parts, s->part, s->st, 1);
+        cg_ref_combine<M><<<1, 1, 0, st>>>(s->part, s->parts, s->st, 2, h, use_cond);
+    }
+    cg_xpay<M><<<tiles, TILE_THREADS, 0, st>>>(s->n, s->p, s->r, ld, s->st, h, use_cond);
+    MWCG_CHECK_LAUNCH();
+    return 0;
+}
+
+int enqueue_iteration_mode(mwcg_solver *s, cudaStream_t st, cudaGraphConditionalHandle h, int use_cond) {
+    switch (s->mode) {
+    case FP64: return enqueue_iteration<FP64>(s, st, h, use_cond);
+    case DW: return enqueue_iteration<DW>(s, st, h, use_cond);
+    case QDW: return enqueue_iteration<QDW>(s, st, h, use_cond);
+    case TW: return enqueue_iteration<TW>(s, st, h, use_cond);
+    default: return enqueue_iteration<QTW>(s, st, h, use_cond);
+    }
+}
+
+template <int M>
+int enqueue_init(mwcg_solver *s) {
+    cudaStream_t st = s->stream;
+    const unsigned tiles = (unsigned)s->ntiles;
+    if (s->fused) {
+        cg_init<M, true><<<tiles, TILE_THREADS, 0, st>>>(s->n, s->b, s->q, s->r, s->p, s->n, s->part,
+                                                          s->ntiles, s->st);
+    } else {
+        const unsigned pb = (unsigned)((s->parts + 127) / 128);
+        cg_init<M, false><<<tiles, TILE_THREADS, 0, st>>>(s->n, s->b, s->q, s->r, s->p, s->n, s->part,
+                                                           s->ntiles, s->st);
+        cg_dot_part<M><<<pb, 128, 0, st>>>(s->n, s->r, s->r, s->n, s->parts, s->part, s->st, 0);
+        cg_ref_combine<M><<<1, 1, 0, st>>>(s->part, s->parts, s->st, 0, cudaGraphConditionalHandle{}, 0);
+    }
+    MWCG_CHECK_LAUNCH();
+    return 0;
+}
+
+int build_graph(mwcg_solver *s) {
+    MWCG_CUDA(cudaGraphCreate(&s->graph, 0));
+    MWCG_CUDA(cudaGraphConditionalHandleCreate(&s->cond, s->graph, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = s->cond;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    MWCG_CUDA(cudaGraphAddNode(&node, s->graph, nullptr, 0, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    MWCG_CUDA(cudaStreamBeginCaptureToGraph(s->cap, body, nullptr, nullptr, 0,
+                                            cudaStreamCaptureModeThreadLocal));
+    int rc = enqueue_iteration_mode(s, s->cap, s->cond, 1);
+    cudaGraph_t out_graph;
+    cudaError_t e = cudaStreamEndCapture(s->cap, &out_graph);
+    if (rc) return rc;
+    MWCG_CUDA(e);
+    MWCG_CUDA(cudaGraphInstantiate(&s->exec, s->graph, 0));
+    return 0;
+}
+
+void free_solver(mwcg_solver *s) {
+    if (!s) return;
+    if (s->exec) cudaGraphExecDestroy(s->exec);
+    if (s->graph) cudaGraphDestroy(s->graph);
+    if (s->own_x) cudaFree(s->x);
+    cudaFree(s->r);
+    cudaFree(s->p);
+    cudaFree(s->q);
+    cudaFree(s->part);
+    cudaFree(s->st);
+    cudaFree(s->xt);
+    cudaFree(s->res);
+    cudaFree(s->diff);
+    cudaFree(s->bt);
+    cudaFree(s->mpart);
+    cudaFree(s->mout);
+    cudaFree(s->mticket);
+    if (s->st_host) cudaFreeHost(s->st_host);
+    if (s->kstop_host) cudaFreeHost(s->kstop_host);
+    if (s->mout_host) cudaFreeHost(s->mout_host);
+    for (auto &e : s->ev)
+        if (e) cudaEventDestroy(e);
+    if (s->cap) cudaStreamDestroy(s->cap);
+    delete s;
+}
+
+// TW sum of squares of a 3-plane vector into mout[slot*3 .. +3] (device)
+int tw_sumsq(mwcg_solver *s, const double *v, int slot) {
+    double *out = s->mout + 3 * slot;
+    if (s->fused) return launch_dot_tile(TW, s->n, v, s->n, v, s->n, out, s->mpart, s->mticket, s->stream);
+    return launch_dot_partitions(TW, s->n, v, s->n, v, s->n, 1, out, s->mpart, s->stream);
+}
+
+}  // namespace
+
+extern "C" {
+
+int mwcg_matrix_create(mwcg_matrix **out, int64_t n_rows, int64_t n_cols, int64_t nnz, const void *row_ptr,
+                       const void *col_idx, const double *values, int index_bytes, void *stream) {
+    if (!out) {
+        set_error("null output handle");
+        return MWCG_ERR_VALUE;
+    }
+    SellMatrixOwned *M = nullptr;
+    int rc = sell_create(&M, n_rows, n_cols, nnz, row_ptr, col_idx, values, index_bytes,
+                         (cudaStream_t)stream);
+    if (rc) return rc;
+    *out = new mwcg_matrix{M};
+    return 0;
+}
+
+int mwcg_matrix_destroy(mwcg_matrix *A) {
+    if (A) {
+        sell_destroy(A->M);
+        delete A;
+    }
+    return 0;
+}
+
+int mwcg_matrix_info(const mwcg_matrix *A, int64_t *n_rows, int64_t *n_cols, int64_t *nnz,
+                     int64_t *padded) {
+    if (!A) {
+        set_error("null matrix");
+        return MWCG_ERR_VALUE;
+    }
+    if (n_rows) *n_rows = A->M->view.n_rows;
+    if (n_cols) *n_cols = A->M->view.n_cols;
+    if (nnz) *nnz = A->M->view.nnz;
+    if (padded) *padded = A->M->view.total;
+    return 0;
+}
+
+int mwcg_spmv(int mode, const mwcg_matrix *A, const double *x, int64_t ldx, double *y, int64_t ldy,
+              void *stream) {
+    if (!A || !valid_mode(mode)) {
+        set_error("bad matrix or mode");
+        return MWCG_ERR_VALUE;
+    }
+    return launch_spmv(mode, A->M->view, x, ldx, y, ldy, (cudaStream_t)stream);
+}
+
+int mwcg_solver_create(mwcg_solver **out, const mwcg_matrix *A, const mwcg_solver_config *cfg, double *x,
+                       void *stream) {
+    if (!out || !A || !cfg) {
+        set_error("null argument");
+        return MWCG_ERR_VALUE;
+    }
+    if (!valid_mode(cfg->mode)) {
+        set_error("unknown arithmetic mode %d", cfg->mode);
+        return MWCG_ERR_VALUE;
+    }
+    if (A->M->view.n_rows != A->M->view.n_cols) {
+        set_error("matrix must be square");
+        return MWCG_ERR_VALUE;
+    }
+    if (cfg->reduction == MWCG_RED_PARTITIONS && cfg->partitions < 1) {
+        set_error("partitions must be >= 1");
+        return MWCG_ERR_VALUE;
+    }
+    auto *s = new mwcg_solver();
+    s->A = A->M->view;
+    s->mode = cfg->mode;
+    s->W = words_of(cfg->mode);
+    s->cfg = *cfg;
+    s->n = s->A.n_rows;
+    s->ntiles = num_tiles(s->n);
+    s->fused = cfg->reduction != MWCG_RED_PARTITIONS;
+    s->parts = s->fused ? 1 : cfg->partitions;
+    s->stream = (cudaStream_t)stream;
+    const size_t vbytes = sizeof(double) * (size_t)s->W * (size_t)(s->n > 0 ? s->n : 1);
+    int rc = 0;
+#define TRY(call)                                  \
+    do {                                           \
+        cudaError_t e_ = (call);                   \
+        if (e_ != cudaSuccess) {                   \
+            set_error("%s: %s", #call, cudaGetErrorString(e_)); \
+            free_solver(s);                        \
+            return (int)e_;                        \
+        }                                          \
+    } while (0)
+    if (x) {
+        s->x = x;
+    } else {
+        TRY(cudaMalloc(&s->x, vbytes));
+        s->own_x = true;
+    }
+    TRY(cudaMalloc(&s->r, vbytes));
+    TRY(cudaMalloc(&s->p, vbytes));
+    TRY(cudaMalloc(&s->q, vbytes));
+    int64_t np = s->fused ? (s->ntiles > 0 ? s->ntiles : 1) : s->parts;
+    TRY(cudaMalloc(&s->part, sizeof(double) * 3 * (size_t)np));
+    TRY(cudaMalloc(&s->st, sizeof(CgState)));
+    TRY(cudaMemset(s->st, 0, sizeof(CgState)));
+    TRY(cudaMallocHost(&s->st_host, sizeof(CgState)));
+    TRY(cudaMallocHost(&s->kstop_host, sizeof(long long)));
+    TRY(cudaMallocHost(&s->mout_host, sizeof(double) * 12));
+    TRY(cudaStreamCreateWithFlags(&s->cap, cudaStreamNonBlocking));
+    for (auto &e : s->ev) TRY(cudaEventCreate(&e));
+#undef TRY
+    if (s->n > 0) {
+        rc = build_graph(s);
+        if (rc) {
+            free_solver(s);
+            return rc;
+        }
+    }
+    *out = s;
+    return 0;
+}
+
+int mwcg_solver_destroy(mwcg_solver *s) {
+    free_solver(s);
+    return 0;
+}
+
+// x0 (FP64, nullable) -> x word 0 (kernels.py:62-67); q = A x; init.
+int mwcg_solver_start(mwcg_solver *s, const double *b, double b_norm, const double *x0,
+                      const double *x_star, double epsilon, int64_t max_iterations) {
+    if (!s) {
+        set_error("null solver");
+        return MWCG_ERR_VALUE;
+    }
+    cudaStream_t st = s->stream;
+    s->b = b;
+    s->x_star = x_star;
+    s->norms_ready = false;
+    const size_t vbytes = sizeof(double) * (size_t)s->W * (size_t)s->n;
+    CgState init{};
+    init.b_norm = (b_norm == 0.0) ? 1.0 : b_norm;
+    init.eps = epsilon;
+    init.max_iters = max_iterations;
+    init.k_stop = 0;
+    const bool quasi = (s->mode == QDW || s->mode == QTW);
+    init.norm_r = quasi && s->cfg.normalization != MWCG_NORM_NONE;
+    init.norm_all = quasi && s->cfg.normalization == MWCG_NORM_EVERY_OP;
+    init.status = RUNNING;
+    *s->st_host = init;
+    MWCG_CUDA(cudaMemcpyAsync(s->st, s->st_host, sizeof(CgState), cudaMemcpyHostToDevice, st));
+    if (s->n == 0) {
+        // empty system: rho = 0 -> rel = 0 < eps -> converged at 0
+        s->st_host->status = CONVERGED;
+        s->st_host->rel = 0.0;
+        MWCG_CUDA(cudaMemcpyAsync(s->st, s->st_host, sizeof(CgState), cudaMemcpyHostToDevice, st));
+        return 0;
+    }
+    MWCG_CUDA(cudaMemsetAsync(s->x, 0, vbytes, st));
+    if (x0) MWCG_CUDA(cudaMemcpyAsync(s->x, x0, sizeof(double) * (size_t)s->n, cudaMemcpyDeviceToDevice, st));
+    int rc = launch_spmv(s->mode, s->A, s->x, s->n, s->q, s->n, st);
+    if (rc) return rc;
+    switch (s->mode) {
+    case FP64: rc = enqueue_init<FP64>(s); break;
+    case DW: rc = enqueue_init<DW>(s); break;
+    case QDW: rc = enqueue_init<QDW>(s); break;
+    case TW: rc = enqueue_init<TW>(s); break;
+    default: rc = enqueue_init<QTW>(s); break;
+    }
+    return rc;
+}
+
+// Run iterations until the solve stops or k == k_stop (async on the stream).
+int mwcg_solver_run(mwcg_solver *s, int64_t k_stop) {
+    if (!s) {
+        set_error("null solver");
+        return MWCG_ERR_VALUE;
+    }
+    if (s->n == 0) return 0;
+    cudaStream_t st = s->stream;
+    // k_stop lives in device state; written from pinned memory (stream-ordered)
+    MWCG_CUDA(cudaStreamSynchronize(st));
+    *s->kstop_host = (long long)k_stop;
+    MWCG_CUDA(cudaMemcpyAsync(&s->st->k_stop, s->kstop_host, sizeof(long long), cudaMemcpyHostToDevice, st));
+    MWCG_CUDA(cudaGraphLaunch(s->exec, st));
+    return 0;
+}
+
+// Same as run, but one kernel launch at a time with CUDA events around each
+// stage; accumulates device milliseconds into ms[0..2] = K1, K2, K3 (fused)
+// or K1, K2, K3 incl. the reference dots (partitions mode).
+int mwcg_solver_run_profiled(mwcg_solver *s, int64_t k_stop, double *ms) {
+    if (!s) {
+        set_error("null solver");
+        return MWCG_ERR_VALUE;
+    }
+    if (s->n == 0) return 0;
+    cudaStream_t st = s->stream;
+    MWCG_CUDA(cudaStreamSynchronize(st));
+    *s->kstop_host = (long long)k_stop;
+    MWCG_CUDA(cudaMemcpyAsync(&s->st->k_stop, s->kstop_host, sizeof(long long), cudaMemcpyHostToDevice, st));
+    MWCG_CUDA(cudaMemcpyAsync(s->st_host, s->st, sizeof(CgState), cudaMemcpyDeviceToHost, st));
+    MWCG_CUDA(cudaStreamSynchronize(st));
+    const unsigned tiles = (unsigned)s->ntiles;
+    cudaGraphConditionalHandle h{};
+    while (s->st_host->status == RUNNING && s->st_host->k < k_stop) {
+        MWCG_CUDA(cudaEventRecord(s->ev[0], st));
+#define STAGES(Mx)                                                                                         \
+    do {                                                                                                   \
+        const unsigned pb = (unsigned)((s->parts + 127) / 128);                                            \
+        if (s->fused) {                                                                                    \
+            cg_spmv_pq<Mx, true><<<tiles, TILE_THREADS, 0, st>>>(s->A, s->p, s->q, s->n, s->part,          \
+                                                                  s->ntiles, s->st, h, 0);                 \
+        } else {                                                                                           \
+            cg_spmv_pq<Mx, false><<<tiles, TILE_THREADS, 0, st>>>(s->A, s->p, s->q, s->n, s->part,         \
+                                                                   s->ntiles, s->st, h, 0);                \
+            cg_dot_part<Mx><<<pb, 128, 0, st>>>(s->n, s->p, s->q, s->n, s->parts, s->part, s->st, 1);      \
+            cg_ref_combine<Mx><<<1, 1, 0, st>>>(s->part, s->parts, s->st, 1, h, 0);                        \
+        }                                                                                                  \
+        cudaEventRecord(s->ev[1], st);                                                                     \
+        if (s->fused) {                                                                                    \
+            cg_update<Mx, true><<<tiles, TILE_THREADS, 0, st>>>(s->n, s->x, s->r, s->p, s->q, s->n,        \
+                                                                 s->part, s->ntiles, s->st, h, 0);         \
+        } else {                                                                                           \
+            cg_update<Mx, false><<<tiles, TILE_THREADS, 0, st>>>(s->n, s->x, s->r, s->p, s->q, s->n,       \
+                                                                  s->part, s->ntiles, s->st, h, 0);        \
+            cg_dot_part<Mx><<<pb, 128, 0, st>>>(s->n, s->r, s->r, s->n, s->parts, s->part, s->st, 1);      \
+            cg_ref_combine<Mx><<<1, 1, 0, st>>>(s->part, s->parts, s->st, 2, h, 0);                        \
+        }                                                                                                  \
+        cudaEventRecord(s->ev[2], st);                                                                     \
+        cg_xpay<Mx><<<tiles, TILE_THREADS, 0, st>>>(s->n, s->p, s->r, s->n, s->st, h, 0);                 \
+    } while (0)
+        switch (s->mode) {
+        case FP64: STAGES(FP64); break;
+        case DW: STAGES(DW); break;
+        case QDW: STAGES(QDW); break;
+        case TW: STAGES(TW); break;
+        default: STAGES(QTW); break;
+        }
+#undef STAGES
+        MWCG_CHECK_LAUNCH();
+        MWCG_CUDA(cudaEventRecord(s->ev[3], st));
+        MWCG_CUDA(cudaMemcpyAsync(s->st_host, s->st, sizeof(CgState), cudaMemcpyDeviceToHost, st));
+        MWCG_CUDA(cudaStreamSynchronize(st));
+        float a = 0, b = 0, c = 0;
+        cudaEventElapsedTime(&a, s->ev[0], s->ev[1]);
+        cudaEventElapsedTime(&b, s->ev[1], s->ev[2]);
+        cudaEventElapsedTime(&c, s->ev[2], s->ev[3]);
+        if (ms) {
+            ms[0] += a;
+            ms[1] += b;
+            ms[2] += c;
+        }
+    }
+    return 0;
+}
+
+int mwcg_solver_state(mwcg_solver *s, mwcg_state *out) {
+    if (!s || !out) {
+        set_error("null argument");
+        return MWCG_ERR_VALUE;
+    }
+    MWCG_CUDA(cudaMemcpyAsync(s->st_host, s->st, sizeof(CgState), cudaMemcpyDeviceToHost, s->stream));
+    MWCG_CUDA(cudaStreamSynchronize(s->stream));
+    const CgState &h = *s->st_host;
+    out->k = h.k;
+    out->status = h.status;
+    out->iterations = h.status == RUNNING ? h.k : h.iterations;
+    out->rel = h.rel;
+    for (int i = 0; i < 3; i++) {
+        out->rho[i] = h.rho[i];
+        out->alpha[i] = h.alpha[i];
+        out->beta[i] = h.beta[i];
+    }
+    return 0;
+}
+
+// TW-accurate error norm and true residual of the current x
+// (norm_metrics_tw, kernels.py:305-328).  *err is NaN when x_star is null.
+int mwcg_solver_metrics(mwcg_solver *s, double *err, double *true_res) {
+    if (!s) {
+        set_error("null solver");
+        return MWCG_ERR_VALUE;
+    }
+    cudaStream_t st = s->stream;
+    const int64_t n = s->n;
+    if (n == 0) {
+        if (err) *err = s->x_star ? 0.0 : NAN;
+        if (true_res) *true_res = 0.0;
+        return 0;
+    }
+    const size_t b3 = sizeof(double) * 3 * (size_t)n;
+    if (!s->xt) {
+        MWCG_CUDA(cudaMalloc(&s->xt, b3));
+        MWCG_CUDA(cudaMalloc(&s->res, b3));
+        MWCG_CUDA(cudaMalloc(&s->diff, b3));
+        MWCG_CUDA(cudaMalloc(&s->bt, b3));
+        MWCG_CUDA(cudaMalloc(&s->mpart, sizeof(double) * 3 * (size_t)(s->ntiles > 0 ? s->ntiles : 1)));
+        MWCG_CUDA(cudaMalloc(&s->mout, sizeof(double) * 12));
+        MWCG_CUDA(cudaMalloc(&s->mticket, sizeof(unsigned int)));
+        MWCG_CUDA(cudaMemset(s->mticket, 0, sizeof(unsigned int)));
+    }
+    const unsigned eb = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16);
+    int rc;
+    if (!s->norms_ready) {
+        promote_fp64_kernel<<<eb, 256, 0, st>>>(n, s->b, s->bt);
+        if ((rc = tw_sumsq(s, s->bt, 2))) return rc;
+        if (s->x_star) {
+            promote_fp64_kernel<<<eb, 256, 0, st>>>(n, s->x_star, s->bt);
+            if ((rc = tw_sumsq(s, s->bt, 3))) return rc;
+        }
+    }
+    switch (s->mode) {
+    case FP64: promote_kernel<FP64><<<eb, 256, 0, st>>>(n, s->x, n, s->xt); break;
+    case DW: promote_kernel<DW><<<eb, 256, 0, st>>>(n, s->x, n, s->xt); break;
+    case QDW: promote_kernel<QDW><<<eb, 256, 0, st>>>(n, s->x, n, s->xt); break;
+    case TW: promote_kernel<TW><<<eb, 256, 0, st>>>(n, s->x, n, s->xt); break;
+    default: promote_kernel<QTW><<<eb, 256, 0, st>>>(n, s->x, n, s->xt); break;
+    }
+    metrics_vec_kernel<<<eb, TILE_THREADS, 0, st>>>(s->A, s->xt, s->b, s->x_star, s->res, s->diff);
+    MWCG_CHECK_LAUNCH();
+    if ((rc = tw_sumsq(s, s->res, 0))) return rc;
+    if (s->x_star && (rc = tw_sumsq(s, s->diff, 1))) return rc;
+    MWCG_CUDA(cudaMemcpyAsync(s->mout_host, s->mout, sizeof(double) * 12, cudaMemcpyDeviceToHost, st));
+    MWCG_CUDA(cudaStreamSynchronize(st));
+    auto coll = [](const double *v) { return (v[0] + v[1]) + v[2]; };
+    if (!s->norms_ready) {
+        s->bnorm_sq = coll(s->mout_host + 6);
+        if (s->bnorm_sq == 0.0) s->bnorm_sq = 1.0;
+        s->xs_sq = s->x_star ? coll(s->mout_host + 9) : 1.0;
+        if (s->xs_sq == 0.0) s->xs_sq = 1.0;
+        s->norms_ready = true;
+    }
+    if (true_res) *true_res = std::sqrt(coll(s->mout_host) / s->bnorm_sq);
+    if (err) *err = s->x_star ? std::sqrt(coll(s->mout_host + 3) / s->xs_sq) : NAN;
+    return 0;
+}
+
+// The whole cg_solve loop (cg.py:78-183) with history records every
+// `history_stride` iterations plus the start / end records.  History arrays
+// are host memory of capacity hist_cap; *n_hist receives the record count
+// (may exceed hist_cap: extra records are counted but not stored).
+int mwcg_cg_solve(mwcg_solver *s, const double *b, double b_norm, const double *x0, const double *x_star,
+                  double epsilon, int64_t max_iterations, int64_t history_stride, int profile,
+                  mwcg_solve_result *res, int64_t hist_cap, int64_t *h_k, double *h_rel,
+                  double *h_true, double *h_err) {
+    if (!s || !res) {
+        set_error("null argument");
+        return MWCG_ERR_VALUE;
+    }
+    if (history_stride < 1) {
+        set_error("history_stride must be >= 1");
+        return MWCG_ERR_VALUE;
+    }
+    int rc = mwcg_solver_start(s, b, b_norm, x0, x_star, epsilon, max_iterations);
+    if (rc) return rc;
+    mwcg_state stt{};
+    if ((rc = mwcg_solver_state(s, &stt))) return rc;
+    int64_t nh = 0, last_rec = -1;
+    double loop_ms = 0.0, hist_ms = 0.0;
+    double stage_ms[3] = {0, 0, 0};
+    auto record = [&](int64_t k, double rel) -> int {
+        double e = NAN, t = NAN;
+        cudaEventRecord(s->ev[4], s->stream);
+        int r2 = mwcg_solver_metrics(s, &e, &t);
+        if (r2) return r2;
+        cudaEventRecord(s->ev[5], s->stream);
+        cudaEventSynchronize(s->ev[5]);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, s->ev[4], s->ev[5]);
+        hist_ms += ms;
+        if (nh < hist_cap) {
+            h_k[nh] = k;
+            h_rel[nh] = rel;
+            h_true[nh] = t;
+            h_err[nh] = e;
+        }
+        nh++;
+        last_rec = k;
+        return 0;
+    };
+    if ((rc = record(0, stt.rel))) return rc;
+    while (stt.status == RUNNING) {
+        int64_t next = (stt.k / history_stride + 1) * history_stride;
+        if (next > max_iterations) next = max_iterations;
+        if (profile) {
+            if ((rc = mwcg_solver_run_profiled(s, next, stage_ms))) return rc;
+        } else {
+            MWCG_CUDA(cudaEventRecord(s->ev[6], s->stream));
+            if ((rc = mwcg_solver_run(s, next))) return rc;
+            MWCG_CUDA(cudaEventRecord(s->ev[7], s->stream));
+        }
+        if ((rc = mwcg_solver_state(s, &stt))) return rc;
+        if (!profile) {
+            float ms = 0;
+            cudaEventElapsedTime(&ms, s->ev[6], s->ev[7]);
+            loop_ms += ms;
+        }
+        if (stt.k % history_stride == 0 && stt.k != last_rec && stt.k > 0 &&
+            (stt.status == RUNNING || stt.iterations == stt.k)) {
+            if ((rc = record(stt.k, stt.rel))) return rc;
+        }
+    }
+    if (last_rec != stt.iterations) {
+        if ((rc = record(stt.iterations, stt.rel))) return rc;
+    }
+    res->iterations = stt.iterations;
+    res->status = stt.status;
+    res->final_rel = stt.rel;
+    res->n_hist = nh;
+    res->loop_ms = profile ? (stage_ms[0] + stage_ms[1] + stage_ms[2]) : loop_ms;
+    res->history_ms = hist_ms;
+    res->stage_ms[0] = stage_ms[0];
+    res->stage_ms[1] = stage_ms[1];
+    res->stage_ms[2] = stage_ms[2];
+    return 0;
+}
+
+}  // extern "C"

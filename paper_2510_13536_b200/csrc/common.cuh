@@ -1,0 +1,164 @@
+// common.cuh -- shared device structures: SELL-32 matrix, CG state, the
+// canonical tile-tree reduction, error plumbing.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include "mw.cuh"
+
+namespace mwcg {
+
+// ---------------------------------------------------------------------------
+// Canonical tile shape.  A tile is TILE_THREADS
+// threads x TILE_ELEMS elements; thread t of tile b owns elements
+// b*TILE + j*TILE_THREADS + t, j = 0..TILE_ELEMS-1 (coalesced).  Every fused
+// dot follows this order, and oracle/mwcg_oracle.c:tile_tree_dot_impl
+// reproduces it bit-for-bit on the CPU.
+// ---------------------------------------------------------------------------
+constexpr int TILE_THREADS = 256;
+constexpr int TILE_ELEMS = 4;
+constexpr int TILE = TILE_THREADS * TILE_ELEMS;
+constexpr int SLICE = 32;  // SELL slice height = one warp
+
+inline int64_t num_tiles(int64_t n) { return (n + TILE - 1) / TILE; }
+
+// SELL-32 matrix (built on device from CSR, sell.cu).  Entry k of row r sits
+// at slice_ptr[r/32] + k*32 + r%32 (column-major inside a slice), so a warp
+// walking its 32 rows in lock-step issues coalesced 128-B/256-B loads while
+// each thread keeps the reference's strict left-to-right order inside its row
+// (kernels.py:175-180).  Padding slots are never read (loop bound row_len).
+struct SellMatrix {
+    int64_t n_rows;
+    int64_t n_cols;
+    int64_t nnz;
+    int64_t n_slices;
+    int64_t total;          // padded entry count
+    const int64_t *slice_ptr;
+    const int32_t *row_len;
+    const int32_t *cols;
+    const double *vals;
+};
+
+// Solver status (cg.py:138-183 reasons)
+enum Status : int { RUNNING = 0, CONVERGED = 1, MAX_ITERS = 2, BREAKDOWN = 3 };
+
+// Device-resident CG scalar state.  All scalars live in the mode's
+// arithmetic (rho, alpha, beta: cg.py:118-181), padded to 3 words.
+struct CgState {
+    double rho[3];
+    double rho_new[3];
+    double pq[3];
+    double alpha[3];
+    double neg_alpha[3];
+    double beta[3];
+    double rel;          // ||r||/||b|| FP64 collapse (cg.py:125-127)
+    double b_norm;       // norm2_fp64(b), 0 -> 1 (cg.py:121-123)
+    double eps;
+    long long k;         // completed iterations
+    long long k_stop;    // pause point (history records)
+    long long max_iters;
+    long long iterations;  // reported count when status != RUNNING
+    int status;
+    int norm_r;          // normalize r (quasi & policy != none)
+    int norm_all;        // every-op normalization
+    int pad0;
+    unsigned int ticket[4];  // last-block-done counters
+    double metrics[4];   // err^2 sum, res^2 sum (collapsed), bnorm_sq, xs_sq
+};
+
+// ---------------------------------------------------------------------------
+// Tree helpers.  Warp: lane l <- add(lane l, lane l+off), off = 16..1.  Block:
+// the same over the TILE_THREADS/32 warp results.  Result valid in thread 0.
+// ---------------------------------------------------------------------------
+template <int M>
+__device__ __forceinline__ mw::V<mw::Arith<M>::W> warp_tree(mw::V<mw::Arith<M>::W> v) {
+    using A = mw::Arith<M>;
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+        auto o = mw::shfl_down<A::W>(v, off);
+        v = A::add(v, o);
+    }
+    return v;
+}
+
+template <int M, int NT>
+__device__ __forceinline__ mw::V<mw::Arith<M>::W> block_tree(mw::V<mw::Arith<M>::W> v,
+                                                             double *smem /* W*NT/32 */) {
+    using A = mw::Arith<M>;
+    constexpr int W = A::W;
+    constexpr int NW = NT / 32;
+    v = warp_tree<M>(v);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < W; k++) smem[k * NW + wid] = v.w[k];
+    }
+    __syncthreads();
+    if (wid == 0) {
+        mw::V<W> u = mw::zero<W>();
+        if (lane < NW) {
+#pragma unroll
+            for (int k = 0; k < W; k++) u.w[k] = smem[k * NW + lane];
+        }
+#pragma unroll
+        for (int off = NW / 2; off >= 1; off >>= 1) {
+            auto o = mw::shfl_down<W>(u, off);
+            u = A::add(u, o);
+        }
+        v = u;
+    }
+    __syncthreads();
+    return v;
+}
+
+// Second pass over ntiles partials (SoA, leading dim ld) by one block of
+// TILE_THREADS threads; identical procedure to a tile with E=ceil(ntiles/TB).
+// Partials written by other CTAs in this grid are read with ld.cg (L2) loads.
+template <int M>
+__device__ __forceinline__ mw::V<mw::Arith<M>::W> reduce_partials_block(const double *part, int64_t ld,
+                                                                         int64_t ntiles, double *smem) {
+    using A = mw::Arith<M>;
+    constexpr int W = A::W;
+    mw::V<W> acc = mw::zero<W>();
+    for (int64_t idx = threadIdx.x; idx < ntiles; idx += TILE_THREADS) {
+        mw::V<W> t;
+#pragma unroll
+        for (int k = 0; k < W; k++) t.w[k] = __ldcg(part + k * ld + idx);
+        acc = A::add(acc, t);
+    }
+    return block_tree<M, TILE_THREADS>(acc, smem);
+}
+
+// Last-block-done election: returns true in every thread of the block that
+// finished last.  The caller must have stored its partial before calling.
+__device__ __forceinline__ bool last_block_done(unsigned int *ticket, int *s_flag) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        unsigned int t = atomicAdd(ticket, 1u);
+        *s_flag = (t == gridDim.x - 1) ? 1 : 0;
+    }
+    __syncthreads();
+    bool last = *s_flag != 0;
+    if (last) __threadfence();
+    return last;
+}
+
+}  // namespace mwcg
+
+// ---------------------------------------------------------------------------
+// error plumbing for the C ABI
+// ---------------------------------------------------------------------------
+namespace mwcg {
+void set_error(const char *fmt, ...);
+}
+#define MWCG_CUDA(call)                                                             \
+    do {                                                                            \
+        cudaError_t e_ = (call);                                                    \
+        if (e_ != cudaSuccess) {                                                    \
+            ::mwcg::set_error("%s:%d %s: %s", __FILE__, __LINE__, #call,            \
+                              cudaGetErrorString(e_));                              \
+            return (int)e_;                                                         \
+        }                                                                           \
+    } while (0)
+#define MWCG_CHECK_LAUNCH() MWCG_CUDA(cudaGetLastError())

@@ -1,0 +1,427 @@
+// mw.cuh -- multi-word FP64 arithmetic for sm_100a (device, register-resident).
+//
+// Bit-exact restatement of the reference scalar algorithms:
+//   EFTs                      _fast.py:41-60        (eft.py:78-122)
+//   DW / QDW add, mul, mixed  _fast.py:63-126       (multiword.py:101-168)
+//   TW / QTW add, mul, mixed  _fast.py:129-277      (multiword.py:175-323)
+//   division                  multiword.py:360-409
+//
+// REQUIRED compile flags: -fmad=false (no contraction: the reference kernels
+// are unfused and TwoProd's p=a*b must not fuse into a later add), no
+// --use_fast_math (IEEE div/sqrt).  Fused operations are explicit __fma_rn.
+//
+// The TW operations are branchy in the reference (3+3 magnitude merge, VecSum,
+// VSEB with data-dependent early exit).  Here they are unrolled register code
+// with selects: no local-memory arrays, identical results including the
+// tie rule (ties take the FIRST operand, _fast.py:186).
+#pragma once
+#include <cstdint>
+
+namespace mw {
+
+enum Mode : int { FP64 = 0, DW = 1, QDW = 2, TW = 3, QTW = 4 };
+
+__host__ __device__ constexpr int words_of(int m) { return m == FP64 ? 1 : (m <= QDW ? 2 : 3); }
+
+template <int W>
+struct V {
+    double w[W];
+};
+
+#define MWI __device__ __forceinline__
+
+// --------------------------------------------------------------- EFTs
+MWI void two_sum(double a, double b, double &x, double &y) {
+    double s = __dadd_rn(a, b);
+    double z = __dsub_rn(s, a);
+    y = __dadd_rn(__dsub_rn(a, __dsub_rn(s, z)), __dsub_rn(b, z));
+    x = s;
+}
+MWI void quick_two_sum(double a, double b, double &x, double &y) {
+    double s = __dadd_rn(a, b);
+    y = __dadd_rn(__dsub_rn(a, s), b);
+    x = s;
+}
+MWI void two_prod(double a, double b, double &x, double &y) {
+    double p = __dmul_rn(a, b);
+    y = __fma_rn(a, b, -p);
+    x = p;
+}
+
+// magnitude compare |a| >= |b| (IEEE: false if either is NaN)
+MWI bool mag_ge(double a, double b) { return fabs(a) >= fabs(b); }
+
+// ------------------------------------------------------------ DW / QDW
+MWI V<2> dw_add(V<2> a, V<2> b) {
+    double s, e;
+    two_sum(a.w[0], b.w[0], s, e);
+    e = __dadd_rn(__dadd_rn(e, a.w[1]), b.w[1]);
+    V<2> r;
+    quick_two_sum(s, e, r.w[0], r.w[1]);
+    return r;
+}
+MWI V<2> qdw_add(V<2> a, V<2> b) {
+    double s, e;
+    two_sum(a.w[0], b.w[0], s, e);
+    e = __dadd_rn(__dadd_rn(e, a.w[1]), b.w[1]);
+    return V<2>{{s, e}};
+}
+MWI V<2> dw_mul(V<2> a, V<2> b) {
+    double p, e;
+    two_prod(a.w[0], b.w[0], p, e);
+    e = __fma_rn(a.w[0], b.w[1], e);
+    e = __fma_rn(a.w[1], b.w[0], e);
+    V<2> r;
+    quick_two_sum(p, e, r.w[0], r.w[1]);
+    return r;
+}
+MWI V<2> qdw_mul(V<2> a, V<2> b) {
+    double p, e;
+    two_prod(a.w[0], b.w[0], p, e);
+    e = __fma_rn(a.w[0], b.w[1], e);
+    e = __fma_rn(a.w[1], b.w[0], e);
+    return V<2>{{p, e}};
+}
+MWI V<2> dxdw_mul(double a, V<2> b) {
+    double p, e;
+    two_prod(a, b.w[0], p, e);
+    e = __fma_rn(a, b.w[1], e);
+    V<2> r;
+    quick_two_sum(p, e, r.w[0], r.w[1]);
+    return r;
+}
+MWI V<2> dxqdw_mul(double a, V<2> b) {
+    double p, e;
+    two_prod(a, b.w[0], p, e);
+    e = __fma_rn(a, b.w[1], e);
+    return V<2>{{p, e}};
+}
+MWI V<2> dxdw_add(double a, V<2> b) {
+    double s, e;
+    two_sum(a, b.w[0], s, e);
+    e = __dadd_rn(e, b.w[1]);
+    V<2> r;
+    quick_two_sum(s, e, r.w[0], r.w[1]);
+    return r;
+}
+MWI V<2> dxqdw_add(double a, V<2> b) {
+    double s, e;
+    two_sum(a, b.w[0], s, e);
+    e = __dadd_rn(e, b.w[1]);
+    return V<2>{{s, e}};
+}
+// _norm_dw: _fast.py:121-126
+MWI V<2> norm_dw(V<2> a) {
+    V<2> r;
+    if (mag_ge(a.w[0], a.w[1])) quick_two_sum(a.w[0], a.w[1], r.w[0], r.w[1]);
+    else two_sum(a.w[0], a.w[1], r.w[0], r.w[1]);
+    return r;
+}
+
+// ------------------------------------------------------------ TW / QTW
+// VSEB_m over an error-free chain e[0..N-1] (_fast.py:136-163,
+// multiword.py:187-203): emit rounded partial sums whenever the running
+// error is non-zero; stop after m words.
+template <int N, int M>
+MWI V<3> vseb(const double (&e)[N]) {
+    double r0 = 0.0, r1 = 0.0, r2 = 0.0;
+    int j = 0;
+    bool done = false;
+    double eps = e[0];
+#pragma unroll
+    for (int i = 0; i < N - 1; i++) {
+        if (!done) {
+            double rj, en;
+            two_sum(eps, e[i + 1], rj, en);
+            if (en != 0.0) {
+                if (j == 0) r0 = rj;
+                else if (j == 1) r1 = rj;
+                else r2 = rj;
+                if (j == M - 1) done = true;
+                j++;
+                eps = en;
+            } else {
+                eps = rj;
+            }
+        }
+    }
+    if (!done) {
+        if (j == 0) r0 = eps;
+        else if (j == 1) r1 = eps;
+        else r2 = eps;
+    }
+    return V<3>{{r0, r1, r2}};
+}
+
+// _vec_sum: multiword.py:175-184 (bottom-up chained TwoSum)
+template <int N>
+MWI void vec_sum(const double (&z)[N], double (&e)[N]) {
+    double s = z[N - 1];
+#pragma unroll
+    for (int k = N - 2; k >= 0; k--) {
+        double err;
+        two_sum(z[k], s, s, err);
+        e[k + 1] = err;
+    }
+    e[0] = s;
+}
+
+// _vecsum3: _fast.py:129-133 (top-down; the QTW normalization)
+MWI V<3> vecsum3(V<3> a) {
+    V<3> r;
+    double c1;
+    two_sum(a.w[0], a.w[1], r.w[0], c1);
+    two_sum(c1, a.w[2], r.w[1], r.w[2]);
+    return r;
+}
+
+// _renorm3: _fast.py:166-175
+MWI V<3> renorm3(double c0, double c1, double c2) {
+    double z[3] = {c0, c1, c2}, e[3];
+    vec_sum<3>(z, e);
+    return vseb<3, 3>(e);
+}
+
+// _tw_add: _fast.py:178-198.  Two-pointer merge by magnitude (not a sort:
+// it reproduces the reference's path exactly, inputs need not be ordered).
+MWI V<3> tw_add(V<3> a, V<3> b) {
+    double z[6];
+    int i = 0, j = 0;
+#pragma unroll
+    for (int k = 0; k < 6; k++) {
+        double ca = (i == 0) ? a.w[0] : ((i == 1) ? a.w[1] : a.w[2]);
+        double cb = (j == 0) ? b.w[0] : ((j == 1) ? b.w[1] : b.w[2]);
+        bool take_a = (i < 3) && ((j >= 3) || mag_ge(ca, cb));
+        z[k] = take_a ? ca : cb;
+        i += take_a ? 1 : 0;
+        j += take_a ? 0 : 1;
+    }
+    double e[6];
+    vec_sum<6>(z, e);
+    return vseb<6, 3>(e);
+}
+// _qtw_add: _fast.py:201-207
+MWI V<3> qtw_add(V<3> a, V<3> b) {
+    double c0, e1, c1, e2, e3;
+    two_sum(a.w[0], b.w[0], c0, e1);
+    two_sum(a.w[1], b.w[1], c1, e2);
+    two_sum(c1, e1, c1, e3);
+    double c2 = __dadd_rn(__dadd_rn(__dadd_rn(a.w[2], b.w[2]), e2), e3);
+    return V<3>{{c0, c1, c2}};
+}
+// _tw_mul: _fast.py:210-218
+MWI V<3> tw_mul(V<3> a, V<3> b) {
+    double c0, e1, t2, e2, t3, e3, c1, e4, e5;
+    two_prod(a.w[0], b.w[0], c0, e1);
+    two_prod(a.w[0], b.w[1], t2, e2);
+    two_prod(a.w[1], b.w[0], t3, e3);
+    two_sum(t2, t3, c1, e4);
+    two_sum(c1, e1, c1, e5);
+    double c2 = __dadd_rn(
+        __fma_rn(a.w[1], b.w[1], __dadd_rn(__fma_rn(a.w[2], b.w[0], e2), __fma_rn(a.w[0], b.w[2], e3))),
+        __dadd_rn(e4, e5));
+    return renorm3(c0, c1, c2);
+}
+// _qtw_mul: _fast.py:221-229
+MWI V<3> qtw_mul(V<3> a, V<3> b) {
+    double c0, e1, t2, e2, t3, e3, c1, e4, e5;
+    two_prod(a.w[0], b.w[0], c0, e1);
+    two_prod(a.w[0], b.w[1], t2, e2);
+    two_prod(a.w[1], b.w[0], t3, e3);
+    two_sum(t2, t3, c1, e4);
+    two_sum(c1, e1, c1, e5);
+    double c2 = __dadd_rn(
+        __dadd_rn(__dadd_rn(__fma_rn(a.w[2], b.w[0], e2), __fma_rn(a.w[1], b.w[1], e3)),
+                  __fma_rn(a.w[0], b.w[2], e4)),
+        e5);
+    return V<3>{{c0, c1, c2}};
+}
+// _dxqtw_mul: _fast.py:232-238
+MWI V<3> dxqtw_mul(double a, V<3> b) {
+    double c0, e1, c1, e2, e5;
+    two_prod(a, b.w[0], c0, e1);
+    two_prod(a, b.w[1], c1, e2);
+    two_sum(c1, e1, c1, e5);
+    return V<3>{{c0, c1, __dadd_rn(__fma_rn(a, b.w[2], e2), e5)}};
+}
+// _dxtw_mul: _fast.py:241-247
+MWI V<3> dxtw_mul(double a, V<3> b) {
+    double c0, e1, c1, e2, e5;
+    two_prod(a, b.w[0], c0, e1);
+    two_prod(a, b.w[1], c1, e2);
+    two_sum(c1, e1, c1, e5);
+    return renorm3(c0, c1, __dadd_rn(__fma_rn(a, b.w[2], e2), e5));
+}
+// _dxqtw_add: _fast.py:250-255
+MWI V<3> dxqtw_add(double a, V<3> b) {
+    double c0, e1, c1, e3;
+    two_sum(a, b.w[0], c0, e1);
+    two_sum(b.w[1], e1, c1, e3);
+    return V<3>{{c0, c1, __dadd_rn(b.w[2], e3)}};
+}
+// _dxtw_add: _fast.py:258-277.  The single FP64 word is inserted before the
+// first b_j it is >= in magnitude (the two-pointer merge with one element).
+MWI V<3> dxtw_add(double a, V<3> b) {
+    bool g0 = mag_ge(a, b.w[0]);
+    bool g1 = mag_ge(a, b.w[1]);
+    bool g2 = mag_ge(a, b.w[2]);
+    double z[4];
+    // position of a: 0 if g0, 1 if g1, 2 if g2, else 3
+    z[0] = g0 ? a : b.w[0];
+    z[1] = g0 ? b.w[0] : (g1 ? a : b.w[1]);
+    z[2] = (g0 || g1) ? b.w[1] : (g2 ? a : b.w[2]);
+    z[3] = (g0 || g1 || g2) ? b.w[2] : a;
+    double e[4];
+    vec_sum<4>(z, e);
+    return vseb<4, 3>(e);
+}
+
+// ------------------------------------------------------------ division
+// dw_div: multiword.py:370-382 (normalized ops, also used for QDW 408)
+MWI V<2> dw_div(V<2> a, V<2> b) {
+    V<2> bn = norm_dw(b);
+    double bc = __dadd_rn(bn.w[0], bn.w[1]);
+    if (bc == 0.0) return V<2>{{__ddiv_rn(__dadd_rn(a.w[0], a.w[1]), bc), 0.0}};
+    V<2> r = a;
+    double q[3];
+#pragma unroll
+    for (int i = 0; i < 3; i++) {
+        q[i] = __ddiv_rn(r.w[0], bn.w[0]);
+        V<2> t = dxdw_mul(q[i], bn);
+        r = dw_add(r, V<2>{{-t.w[0], -t.w[1]}});
+    }
+    double e[3];
+    vec_sum<3>(q, e);
+    V<3> c = vseb<3, 2>(e);
+    return V<2>{{c.w[0], c.w[1]}};
+}
+// tw_div: multiword.py:385-397, _strict_normalize_tw 400-402
+MWI V<3> tw_div(V<3> a, V<3> b) {
+    double bz[3] = {b.w[0], b.w[1], b.w[2]}, be[3];
+    vec_sum<3>(bz, be);
+    V<3> bn = vseb<3, 3>(be);
+    double bc = __dadd_rn(__dadd_rn(bn.w[0], bn.w[1]), bn.w[2]);
+    if (bc == 0.0)
+        return V<3>{{__ddiv_rn(__dadd_rn(__dadd_rn(a.w[0], a.w[1]), a.w[2]), bc), 0.0, 0.0}};
+    V<3> r = a;
+    double q[4];
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        q[i] = __ddiv_rn(r.w[0], bn.w[0]);
+        V<3> t = dxtw_mul(q[i], bn);
+        r = tw_add(r, V<3>{{-t.w[0], -t.w[1], -t.w[2]}});
+    }
+    double e[4];
+    vec_sum<4>(q, e);
+    return vseb<4, 3>(e);
+}
+
+// ------------------------------------------------------------ mode traits
+template <int M>
+struct Arith;
+
+template <>
+struct Arith<FP64> {
+    static constexpr int W = 1;
+    using T = V<1>;
+    static MWI T add(T a, T b) { return T{{__dadd_rn(a.w[0], b.w[0])}}; }
+    static MWI T mul(T a, T b) { return T{{__dmul_rn(a.w[0], b.w[0])}}; }
+    static MWI T dxmul(double a, T b) { return T{{__dmul_rn(a, b.w[0])}}; }
+    static MWI T dxadd(double a, T b) { return T{{__dadd_rn(a, b.w[0])}}; }
+    static MWI T norm(T a) { return a; }
+    static MWI T div(T a, T b) { return T{{__ddiv_rn(a.w[0], b.w[0])}}; }
+    static MWI double collapse(T a) { return a.w[0]; }
+};
+template <>
+struct Arith<DW> {
+    static constexpr int W = 2;
+    using T = V<2>;
+    static MWI T add(T a, T b) { return dw_add(a, b); }
+    static MWI T mul(T a, T b) { return dw_mul(a, b); }
+    static MWI T dxmul(double a, T b) { return dxdw_mul(a, b); }
+    static MWI T dxadd(double a, T b) { return dxdw_add(a, b); }
+    static MWI T norm(T a) { return a; }
+    static MWI T div(T a, T b) { return dw_div(a, b); }
+    static MWI double collapse(T a) { return __dadd_rn(a.w[0], a.w[1]); }
+};
+template <>
+struct Arith<QDW> {
+    static constexpr int W = 2;
+    using T = V<2>;
+    static MWI T add(T a, T b) { return qdw_add(a, b); }
+    static MWI T mul(T a, T b) { return qdw_mul(a, b); }
+    static MWI T dxmul(double a, T b) { return dxqdw_mul(a, b); }
+    static MWI T dxadd(double a, T b) { return dxqdw_add(a, b); }
+    static MWI T norm(T a) { return norm_dw(a); }
+    static MWI T div(T a, T b) { return dw_div(a, b); }
+    static MWI double collapse(T a) { return __dadd_rn(a.w[0], a.w[1]); }
+};
+template <>
+struct Arith<TW> {
+    static constexpr int W = 3;
+    using T = V<3>;
+    static MWI T add(T a, T b) { return tw_add(a, b); }
+    static MWI T mul(T a, T b) { return tw_mul(a, b); }
+    static MWI T dxmul(double a, T b) { return dxtw_mul(a, b); }
+    static MWI T dxadd(double a, T b) { return dxtw_add(a, b); }
+    static MWI T norm(T a) { return a; }
+    static MWI T div(T a, T b) { return tw_div(a, b); }
+    static MWI double collapse(T a) { return __dadd_rn(__dadd_rn(a.w[0], a.w[1]), a.w[2]); }
+};
+template <>
+struct Arith<QTW> {
+    static constexpr int W = 3;
+    using T = V<3>;
+    static MWI T add(T a, T b) { return qtw_add(a, b); }
+    static MWI T mul(T a, T b) { return qtw_mul(a, b); }
+    static MWI T dxmul(double a, T b) { return dxqtw_mul(a, b); }
+    static MWI T dxadd(double a, T b) { return dxqtw_add(a, b); }
+    static MWI T norm(T a) { return vecsum3(a); }
+    static MWI T div(T a, T b) { return tw_div(a, b); }
+    static MWI double collapse(T a) { return __dadd_rn(__dadd_rn(a.w[0], a.w[1]), a.w[2]); }
+};
+
+template <int W>
+MWI V<W> zero() {
+    V<W> r;
+#pragma unroll
+    for (int k = 0; k < W; k++) r.w[k] = 0.0;
+    return r;
+}
+template <int W>
+MWI V<W> neg(V<W> a) {
+    V<W> r;
+#pragma unroll
+    for (int k = 0; k < W; k++) r.w[k] = -a.w[k];
+    return r;
+}
+
+// SoA word-plane access: word k of element i at v[k*ld + i]
+template <int W>
+MWI V<W> load(const double *__restrict__ v, int64_t ld, int64_t i) {
+    V<W> r;
+#pragma unroll
+    for (int k = 0; k < W; k++) r.w[k] = v[k * ld + i];
+    return r;
+}
+template <int W>
+MWI V<W> load_ro(const double *__restrict__ v, int64_t ld, int64_t i) {
+    V<W> r;
+#pragma unroll
+    for (int k = 0; k < W; k++) r.w[k] = __ldg(v + k * ld + i);
+    return r;
+}
+template <int W>
+MWI void store(double *__restrict__ v, int64_t ld, int64_t i, V<W> a) {
+#pragma unroll
+    for (int k = 0; k < W; k++) v[k * ld + i] = a.w[k];
+}
+template <int W>
+MWI V<W> shfl_down(V<W> a, int off) {
+    V<W> r;
+#pragma unroll
+    for (int k = 0; k < W; k++) r.w[k] = __shfl_down_sync(0xffffffffu, a.w[k], off);
+    return r;
+}
+
+}  // namespace mw

@@ -1,0 +1,45 @@
+// mwcg_internal.h -- declarations shared by the translation units of
+// libmwcg_cuda.so (not part of the public C ABI; see include/mwcg_cuda.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include "common.cuh"
+
+// library error codes (cudaError_t values are returned as-is, all < 1000)
+#define MWCG_ERR_VALUE 1001
+#define MWCG_ERR_STATE 1002
+
+namespace mwcg {
+
+struct SellMatrixOwned {
+    SellMatrix view{};
+    int32_t *row_len = nullptr;
+    int64_t *slice_ptr = nullptr;
+    int32_t *cols = nullptr;
+    double *vals = nullptr;
+};
+
+int sell_create(SellMatrixOwned **out, int64_t n_rows, int64_t n_cols, int64_t nnz,
+                const void *row_ptr, const void *col_idx, const double *values, int index_bytes,
+                cudaStream_t st);
+void sell_destroy(SellMatrixOwned *M);
+
+// operator-level launches (ops.cu); all stream-ordered
+int launch_spmv(int mode, const SellMatrix &A, const double *x, int64_t ldx, double *y, int64_t ldy,
+                cudaStream_t st);
+int launch_dot_tile(int mode, int64_t n, const double *x, int64_t ldx, const double *y, int64_t ldy,
+                    double *out, double *work, unsigned int *ticket, cudaStream_t st);
+int launch_dot_partitions(int mode, int64_t n, const double *x, int64_t ldx, const double *y,
+                          int64_t ldy, int64_t parts, double *out, double *work, cudaStream_t st);
+int launch_axpy(int mode, int64_t n, const double *alpha, const double *x, int64_t ldx, double *y,
+                int64_t ldy, cudaStream_t st);
+int launch_scal_add(int mode, int64_t n, const double *beta, double *p, int64_t ldp, const double *r,
+                    int64_t ldr, cudaStream_t st);
+int launch_residual(int mode, int64_t n, const double *b, const double *q, int64_t ldq, double *r,
+                    int64_t ldr, cudaStream_t st);
+int launch_normalize(int mode, int64_t n, double *v, int64_t ld, cudaStream_t st);
+int launch_scalar_op(int op, int mode, const double *a, const double *b, double *out, cudaStream_t st);
+
+inline bool valid_mode(int m) { return m >= 0 && m <= 4; }
+
+}  // namespace mwcg
