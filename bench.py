@@ -1,0 +1,420 @@
+#!/usr/bin/env python
+"""bench.py -- CG iterations/s and time-to-solution on B200 (BASELINE.json).
+
+Workload (N=1): BASELINE config 2 -- 3-D 7-point Poisson on a 128^3 grid
+(n = 2,097,152, nnz = 14,581,760), b = A*ones, x0 = 0, eps = 1e-12; one
+step = one complete CG solve in the headline arithmetic (DW by default),
+including the solver's start/end TW-accurate history records.  Config 1 is
+CPU-runnable and is a parity-test case (tests/), not a bench line.
+
+  value    : whole-job CG iterations/s with A, b resident in HBM
+  e2e      : the same metric through the public API `cg_solve(A, b)` with
+             HOST inputs in pinned memory: every step re-uploads the CSR
+             matrix (int64 indices, as the reference's CsrMatrix holds them)
+             and b, rebuilds the device SELL layout and graph, solves, and
+             reads the solution words back
+  roofline : K1 (SpMV + fused p.q) -- the dominant kernel
+  per_arithmetic : one timed solve per arithmetic (fp64/dw/qdw/tw/qtw)
+  cpu_baseline   : the C oracle (a port of the reference path) on the host
+                   cores, bounded sample of CG iterations of the same config
+
+`--impl reference` times the reference's CPU path (the oracle port, all host
+threads) on the same config and metric.  Under torchrun (N>1) every rank
+solves its own copy of the problem (replicas; the row-partitioned solver is
+DESIGN.md's multi-GPU section) and value = total iterations / max-over-ranks
+time.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MODES = ("fp64", "dw", "qdw", "tw", "qtw")
+WORDS = {"fp64": 1, "dw": 2, "qdw": 2, "tw": 3, "qtw": 3}
+# FP64 ops per iteration F = f_nnz*nnz + f_n*n
+FLOPS = {"fp64": (2, 10), "dw": (17, 90), "qdw": (11, 63), "tw": (96, 540), "qtw": (33, 237)}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4"])
+    ap.add_argument("--mode", default="dw", choices=MODES)
+    ap.add_argument("--no-per-arith", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def algorithmic_bytes(n, nnz, w):
+    """one CG iteration = A once (f64 + int32 col) + int32
+    row_ptr + 9 vector passes of 8w n bytes."""
+    return 12 * nnz + 4 * (n + 1) + 72 * w * n
+
+
+def k1_bytes(n, nnz, w):
+    """K1 (SpMV + p.q): A once + row descriptors + p gathered once + q written."""
+    return 12 * nnz + 4 * (n + 1) + 16 * w * n
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def load_problem(name):
+    from paper_2510_13536_b200 import problems
+    return problems.CONFIGS[name]()
+
+
+def workload_name(cfg, mode):
+    A = cfg["A"]
+    desc = {"C1": "2-D 5-point Poisson 256^2", "C2": "3-D 7-point Poisson 128^3",
+            "C3": "3-D 27-point stencil 160^3", "C4": "banded ill-conditioned SPD n=1e6"}[cfg["name"]]
+    return f"{cfg['name']} {desc}, CG in {mode.upper()} to {cfg['epsilon']:g} (n={A.n_rows}, nnz={A.nnz})"
+
+
+def cpu_sample(cfg, mode, seconds, threads):
+    """The oracle port (oracle/mwcg_oracle.c, reference algorithm) on the host
+    cores: bounded number of unconditional CG iterations."""
+    from oracle import oracle as orc
+    orc.set_threads(threads)
+    A, b = cfg["A"], cfg["b"]
+    t0 = time.perf_counter()
+    orc.cg_iterations(A, b, mode, 2, partitions=threads)
+    t_it = max((time.perf_counter() - t0) / 2, 1e-6)
+    iters = int(max(3, min(2000, seconds / t_it)))
+    t0 = time.perf_counter()
+    orc.cg_iterations(A, b, mode, iters, partitions=threads)
+    dt = time.perf_counter() - t0
+    return iters, dt
+
+
+# ---------------------------------------------------------------------------
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from oracle import oracle as orc
+    cfg = load_problem(a.config)
+    threads = orc.max_threads()
+    orc.set_threads(threads)
+    per_step = max(1.0, a.cpu_seconds / max(1, a.steps))
+    for _ in range(max(0, min(a.warmup, 1))):
+        cpu_sample(cfg, a.mode, 0.5, threads)
+    tot_it, tot_t = 0, 0.0
+    for _ in range(a.steps):
+        it, dt = cpu_sample(cfg, a.mode, per_step, threads)
+        tot_it += it
+        tot_t += dt
+    v = tot_it / tot_t
+    line = {
+        "impl": "reference", "metric": "CG iterations/s", "value": v, "unit": "iter/s",
+        "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": 1e3 * tot_t / a.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload_name(cfg, a.mode), "mode": a.mode,
+                   "parallelism": f"{threads} host threads"},
+        "cpu_baseline": {"value": v, "unit": "iter/s", "cores": threads, "kind": "port",
+                         "sample": f"{tot_it} unconditional CG iterations of {cfg['name']} in "
+                                   f"{a.mode} (oracle/mwcg_oracle.c, partitions={threads})"},
+        "e2e": {"value": v, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+def run_ours(a):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2510_13536_b200 import cg, kernels, _lib
+    from paper_2510_13536_b200.cg import Solver, _b_norm
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    cfg = load_problem(a.config)
+    A, b, xs = cfg["A"], cfg["b"], cfg["x_star"]
+    n, nnz, mode = A.n_rows, A.nnz, a.mode
+    w = WORDS[mode]
+    eps, max_it = cfg["epsilon"], cfg["max_iterations"]
+    stride = 10 ** 9  # start/end records only (the reference records them too)
+    hbm, hbm_src = peaks()
+    L = _lib.load()
+    import ctypes
+    fp64_ops, fp64_ms = ctypes.c_double(), ctypes.c_double()
+    _lib.check(L.mwcg_fp64_peak(ctypes.byref(fp64_ops), ctypes.byref(fp64_ms), _lib.stream_handle()))
+    fp64_peak = fp64_ops.value  # FP64 ops/s (FMA = 1), measured live
+
+    b_dev = torch.from_numpy(b).cuda()
+    bn = _b_norm(b)
+
+    def device_solve(solver, profile=False):
+        return solver.solve(b_dev, bn, None, None, eps, max_it, stride, profile)
+
+    # ---- value: device-resident inputs ------------------------------------
+    solver = Solver(A, mode)
+    for _ in range(max(3, a.warmup)):
+        device_solve(solver)
+    barrier()
+    iters, launches = 0, 0
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0.record()
+        for _ in range(a.steps):
+            res, _ = device_solve(solver)
+            iters += int(res.iterations)
+            launches += int(res.launches)
+        ev1.record()
+        barrier()
+    dt = ev0.elapsed_time(ev1) * 1e-3
+    dt_max = max_over_ranks(dt)
+    total_iters = sum_over_ranks(iters)
+    value = total_iters / dt_max
+    ms_per_step = 1e3 * dt_max / a.steps
+    reason = _lib.STATUS[res.status]
+    iters_per_solve = int(res.iterations)
+
+    # ---- roofline of K1 (profiled solve: per-stage CUDA events) ------------
+    pres, _ = device_solve(solver, profile=True)
+    it_p = max(1, int(pres.iterations))
+    k1_s = pres.stage_ms[0] * 1e-3 / it_p
+    k2_s = pres.stage_ms[1] * 1e-3 / it_p
+    k3_s = pres.stage_ms[2] * 1e-3 / it_p
+    k1_achieved = k1_bytes(n, nnz, w) / k1_s / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            prof = json.load(f)
+        traffic = prof.get("k1_dram_bytes_per_launch", {}).get(a.config, {}).get(mode)
+    except Exception:
+        pass
+    roofline = {"bound": "hbm", "achieved": k1_achieved, "peak": hbm, "unit": "GB/s",
+                "frac": k1_achieved / hbm, "traffic": traffic,
+                "kernel": "cg_spmv_pq (SpMV + fused p.q + alpha)",
+                "algorithmic_bytes_per_launch": k1_bytes(n, nnz, w),
+                "launch_us": k1_s * 1e6, "peak_source": hbm_src,
+                "stage_us": {"K1_spmv_pq": k1_s * 1e6, "K2_update_rr": k2_s * 1e6,
+                             "K3_xpay": k3_s * 1e6},
+                "iteration": {"us": 1e6 * dt / max(1, iters),
+                              "algorithmic_bytes": algorithmic_bytes(n, nnz, w),
+                              "achieved_gbs": algorithmic_bytes(n, nnz, w) * iters / dt / 1e9,
+                              "frac": algorithmic_bytes(n, nnz, w) * iters / dt / 1e9 / hbm}}
+
+    # ---- per-arithmetic solves (device-resident) -----------------------------
+    per = {}
+    if not a.no_per_arith:
+        for m in MODES:
+            sv = solver if m == mode else Solver(A, m)
+            device_solve(sv)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            r, _ = device_solve(sv)
+            e1.record()
+            torch.cuda.synchronize()
+            t = e0.elapsed_time(e1) * 1e-3
+            it = max(1, int(r.iterations))
+            wm = WORDS[m]
+            B = algorithmic_bytes(n, nnz, wm)
+            fn, fx = FLOPS[m]
+            F = fn * nnz + fx * n
+            bw = B * it / t / 1e9
+            fl = F * it / t
+            hfrac, ffrac = bw / hbm, fl / fp64_peak
+            per[m] = {"iterations": int(r.iterations), "reason": _lib.STATUS[r.status],
+                      "final_rel": r.final_rel, "time_to_solution_s": t,
+                      "iter_per_s": it / t, "us_per_iter": 1e6 * t / it,
+                      "hbm_gbs": bw, "hbm_frac": hfrac, "fp64_tops": fl / 1e12,
+                      "fp64_frac": ffrac, "roofline_frac": max(hfrac, ffrac),
+                      "bound": "fp64" if ffrac > hfrac else "hbm"}
+            if sv is not solver:
+                del sv
+            torch.cuda.empty_cache()
+
+    # ---- e2e through the public API with host inputs -------------------------
+    e2e = None
+    if not a.no_e2e:
+        import torch as _t
+        pin = {k: _t.from_numpy(np.ascontiguousarray(v)).pin_memory()
+               for k, v in (("rp", A.row_ptr), ("ci", A.col_idx), ("va", A.values), ("b", b))}
+        from paper_2510_13536_b200.sparse import CsrMatrix
+        h2d = sum(t.numel() * t.element_size() for t in pin.values())
+        d2h = w * n * 8
+        conf = cg.SolverConfig(mode=mode, epsilon=eps, max_iterations=max_it, history_stride=stride)
+
+        def e2e_step():
+            Ah = CsrMatrix.__new__(CsrMatrix)  # pinned arrays, validated once below
+            object.__setattr__(Ah, "n_rows", n)
+            object.__setattr__(Ah, "n_cols", n)
+            object.__setattr__(Ah, "row_ptr", pin["rp"].numpy())
+            object.__setattr__(Ah, "col_idx", pin["ci"].numpy())
+            object.__setattr__(Ah, "values", pin["va"].numpy())
+            object.__setattr__(Ah, "_device", None)
+            r = cg.cg_solve(Ah, pin["b"].numpy(), conf)
+            xw = r.x.planes.cpu()  # solution words back to the host
+            return r, xw
+
+        CsrMatrix(n, n, A.row_ptr, A.col_idx, A.values)  # validation (not timed)
+        for _ in range(max(1, min(a.warmup, 2))):
+            e2e_step()
+        barrier()
+        t0 = time.perf_counter()
+        e_it = 0
+        for _ in range(a.steps):
+            r, _ = e2e_step()
+            e_it += int(r.iterations)
+        barrier()
+        e_dt = max_over_ranks(time.perf_counter() - t0)
+        e2e = {"value": sum_over_ranks(e_it) / e_dt, "unit": "iter/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": 1e3 * e_dt / a.steps,
+               "path": "cg_solve(CsrMatrix(host, pinned), b host) -> x words to host"}
+
+    # ---- CPU baseline (rank 0, N=1 only) -------------------------------------
+    cpu = None
+    if world == 1 and rank == 0:
+        try:
+            from oracle import oracle as orc
+            thr = orc.max_threads()
+            it, cdt = cpu_sample(cfg, mode, a.cpu_seconds, thr)
+            cpu = {"value": it / cdt, "unit": "iter/s", "cores": thr, "kind": "port",
+                   "sample": f"{it} unconditional CG iterations of {cfg['name']} in {mode} "
+                             f"(oracle/mwcg_oracle.c, partitions={thr}), {cdt:.1f} s"}
+        except Exception as exc:  # pragma: no cover
+            cpu = {"value": None, "unit": "iter/s", "cores": 0, "kind": "port",
+                   "sample": f"unavailable: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": "CG iterations/s", "value": value, "unit": "iter/s", "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_name(cfg, mode), "mode": mode, "n": n, "nnz": nnz,
+                       "epsilon": eps, "iterations_per_solve": iters_per_solve,
+                       "reason": reason, "time_to_solution_s": ms_per_step * 1e-3,
+                       "parallelism": "replicas" if world > 1 else "single",
+                       "l2": f"inputs larger than L2 (A {12 * nnz / 1e6:.0f} MB + vectors "
+                             f"{4 * 8 * w * n / 1e6:.0f} MB > 126 MB)",
+                       "reduction": "canonical tile tree (bitwise-reproducible)"},
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "fp64_peak_tops_measured": fp64_peak / 1e12,
+            "per_arithmetic": per,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        return run_reference(a)
+    return run_ours(a)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -75,6 +75,7 @@ typedef struct {
     double loop_ms;      /* device time of the iteration loop (CUDA events) */
     double history_ms;   /* device time spent in history metrics */
     double stage_ms[3];  /* profile=1 only: K1 spmv+p.q, K2 update+r.r, K3 xpay */
+    int64_t launches;    /* kernels launched by the solve (graph nodes included) */
 } mwcg_solve_result;
 
 /* ---- library ---- */

@@ -7,7 +7,7 @@ import ctypes
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libmwcg_cuda.so")
+LIB_PATH = os.environ.get("MWCG_LIB") or os.path.join(PKG, "libmwcg_cuda.so")
 
 MODES = ("fp64", "dw", "qdw", "tw", "qtw")
 MODE_ID = {m: i for i, m in enumerate(MODES)}
@@ -39,7 +39,7 @@ class SolveResultC(ctypes.Structure):
     _fields_ = [("iterations", c_i64), ("n_hist", c_i64), ("status", ctypes.c_int),
                 ("reserved", ctypes.c_int), ("final_rel", ctypes.c_double),
                 ("loop_ms", ctypes.c_double), ("history_ms", ctypes.c_double),
-                ("stage_ms", ctypes.c_double * 3)]
+                ("stage_ms", ctypes.c_double * 3), ("launches", c_i64)]
 
 
 # name -> (restype, argtypes); every symbol declared in include/mwcg_cuda.h

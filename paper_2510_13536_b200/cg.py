@@ -90,6 +90,7 @@ class SolverResult:
     kernel_seconds: dict = field(default_factory=dict)
     device_seconds: float = 0.0      # CUDA-event time of the iteration loop
     history_seconds: float = 0.0     # CUDA-event time of the history metrics
+    gpu_launches: int = 0            # kernels launched by the solve
 
 
 def _dev_f64(a):
@@ -193,4 +194,5 @@ def cg_solve(A, b, config=SolverConfig(), x0=None, x_star=None, reference=False)
                         iterations=int(res.iterations),
                         final_recurrence_residual=float(res.final_rel), x=x, history=hist,
                         elapsed_seconds=elapsed, kernel_seconds=ks,
-                        device_seconds=res.loop_ms * 1e-3, history_seconds=res.history_ms * 1e-3)
+                        device_seconds=res.loop_ms * 1e-3, history_seconds=res.history_ms * 1e-3,
+                        gpu_launches=int(res.launches))

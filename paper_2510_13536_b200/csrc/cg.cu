@@ -113,36 +113,98 @@ __device__ __forceinline__ bool stopped(const CgState *st, cudaGraphConditionalH
     return false;
 }
 
+// Snake order: each kernel walks the tiles in the direction opposite to the
+// kernel before it, so its first reads hit the lines the previous kernel
+// touched last (still in L2).  Iteration k: SpMV dir = k&1, update = !(k&1),
+// xpay (after k++) = !(k'&1) = k&1.  Reduction order is unaffected (partials
+// are indexed by tile).
+__device__ __forceinline__ int64_t snake(int64_t t, int64_t ntiles, int dir) {
+    return dir ? (ntiles - 1 - t) : t;
+}
+
+// Persistent tile loop: every fused kernel runs grid = min(ntiles, resident
+// CTAs) blocks, block b handling tiles b, b+grid, ...  Partials are indexed by
+// tile, so the reduction order is independent of the grid size.
+//
 // ---------------------------------------------------------------- K1
+// K1: one tile (1024 rows) per CTA of SP_THREADS(M) threads, each thread
+// walking 1024/SP_THREADS rows of the tile (row = tile*1024 + tid + k*THREADS).
+// High occupancy is what keeps enough loads in flight (Little's law; see
+// DESIGN.md "SpMV").  The p.q terms of the tile are staged in shared memory
+// and the canonical tile order (thread t: terms t, t+256, t+512, t+768, then
+// the 256-thread tree) is replayed by the first 256 threads, so the thread
+// mapping of the SpMV is free while the reduction order stays canonical.
+template <int M>
+struct SpTraits {
+#ifdef MWCG_SP_THREADS_OVERRIDE
+    static constexpr int THREADS = MWCG_SP_THREADS_OVERRIDE;
+#else
+    static constexpr int THREADS = 512;
+#endif
+#ifdef MWCG_SP_MINB_OVERRIDE
+    static constexpr int MINB = MWCG_SP_MINB_OVERRIDE;
+#else
+    static constexpr int MINB = (M == FP64) ? 3 : 2;
+#endif
+    static constexpr int RPT = TILE / THREADS;
+};
+
 template <int M, bool FUSED>
-__global__ void __launch_bounds__(TILE_THREADS)
+__global__ void __launch_bounds__(SpTraits<M>::THREADS, SpTraits<M>::MINB)
     cg_spmv_pq(SellMatrix A, const double *__restrict__ p, double *__restrict__ q, int64_t ld,
                double *__restrict__ part, int64_t ntiles, CgState *st, cudaGraphConditionalHandle h,
                int use_cond) {
     using Ar = Arith<M>;
     constexpr int W = Ar::W;
+    constexpr int NT = SpTraits<M>::THREADS;
+    constexpr int RPT = SpTraits<M>::RPT;
+    __shared__ double terms[FUSED ? W * TILE : 1];
     __shared__ double smem[W * TILE_THREADS / 32];
     __shared__ int s_last;
     if (stopped(st, h, use_cond)) return;
     const bool norm_all = st->norm_all != 0;
     const int64_t n = A.n_rows;
-    const int64_t base = (int64_t)blockIdx.x * TILE + threadIdx.x;
-    V<W> acc = zero<W>();
+    const int dir = (int)(st->k & 1);
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int64_t tile = snake(t, ntiles, dir);
 #pragma unroll 1
-    for (int j = 0; j < TILE_ELEMS; j++) {
-        int64_t row = base + j * TILE_THREADS;
-        if (row < n) {
-            V<W> s = spmv_row<M>(A, p, ld, row);
-            if (norm_all) s = Ar::norm(s);
-            store<W>(q, ld, row, s);
-            if (FUSED) acc = Ar::add(acc, Ar::mul(load_ro<W>(p, ld, row), s));
+        for (int k = 0; k < RPT; k++) {
+            const int li = threadIdx.x + k * NT;  // row inside the tile
+            const int64_t row = tile * TILE + li;
+            V<W> term = zero<W>();
+            if (row < n) {
+                V<W> sv = spmv_row<M, 8>(A, p, ld, row);
+                if (norm_all) sv = Ar::norm(sv);
+                store<W>(q, ld, row, sv);
+                if (FUSED) term = Ar::mul(load_ro<W>(p, ld, row), sv);
+            }
+            if (FUSED) {
+#pragma unroll
+                for (int w = 0; w < W; w++) terms[w * TILE + li] = term.w[w];
+            }
+        }
+        if (FUSED) {
+            __syncthreads();
+            V<W> acc = zero<W>();
+            if (threadIdx.x < TILE_THREADS) {
+                const int64_t base = tile * TILE + threadIdx.x;
+#pragma unroll
+                for (int j = 0; j < TILE_ELEMS; j++) {
+                    if (base + j * TILE_THREADS < n) {
+                        V<W> t;
+#pragma unroll
+                        for (int w = 0; w < W; w++) t.w[w] = terms[w * TILE + threadIdx.x + j * TILE_THREADS];
+                        acc = Ar::add(acc, t);
+                    }
+                }
+            }
+            acc = block_tree_first<M, TILE_THREADS>(acc, smem);
+            if (threadIdx.x == 0) store<W>(part, ntiles, tile, acc);
         }
     }
     if (!FUSED) return;
-    acc = block_tree<M, TILE_THREADS>(acc, smem);
-    if (threadIdx.x == 0) store<W>(part, ntiles, blockIdx.x, acc);
     if (!last_block_done(&st->ticket[0], &s_last)) return;
-    V<W> pq = reduce_partials_block<M>(part, ntiles, ntiles, smem);
+    V<W> pq = reduce_partials_first<M>(part, ntiles, ntiles, smem);
     if (threadIdx.x == 0) {
         st->ticket[0] = 0u;
         scalar_alpha<M>(st, pq, h, use_cond);
@@ -150,6 +212,17 @@ __global__ void __launch_bounds__(TILE_THREADS)
 }
 
 // ---------------------------------------------------------------- K2
+// All loads of a tile are issued before any arithmetic (the compiler will not
+// hoist loads of x/r above the stores of the previous element by itself).
+// Loads are hoisted HOIST elements at a time (all loads of a group issue
+// before any arithmetic; the compiler does not hoist loads of x/r above the
+// stores of the previous element by itself).  TW is FP64-bound: no hoisting,
+// registers go to occupancy instead.
+template <int M>
+struct Hoist {
+    static constexpr int value = (M == TW) ? 1 : (Arith<M>::W == 3 ? 2 : TILE_ELEMS);
+};
+
 template <int M, bool FUSED>
 __global__ void __launch_bounds__(TILE_THREADS)
     cg_update(int64_t n, double *__restrict__ x, double *__restrict__ r, const double *__restrict__ p,
@@ -157,6 +230,7 @@ __global__ void __launch_bounds__(TILE_THREADS)
               CgState *st, cudaGraphConditionalHandle h, int use_cond) {
     using Ar = Arith<M>;
     constexpr int W = Ar::W;
+    constexpr int H = Hoist<M>::value;
     __shared__ double smem[W * TILE_THREADS / 32];
     __shared__ int s_last;
     if (stopped(st, h, use_cond)) return;
@@ -167,24 +241,44 @@ __global__ void __launch_bounds__(TILE_THREADS)
         alpha.w[k] = st->alpha[k];
         nalpha.w[k] = st->neg_alpha[k];
     }
-    const int64_t base = (int64_t)blockIdx.x * TILE + threadIdx.x;
-    V<W> acc = zero<W>();
+    const int dir = (int)((st->k & 1) ^ 1);
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int64_t tile = snake(t, ntiles, dir);
+        const int64_t base = tile * TILE + threadIdx.x;
+        V<W> acc = zero<W>();
 #pragma unroll
-    for (int j = 0; j < TILE_ELEMS; j++) {
-        int64_t i = base + j * TILE_THREADS;
-        if (i < n) {
-            V<W> xi = Ar::add(load<W>(x, ld, i), Ar::mul(alpha, load_ro<W>(p, ld, i)));
-            if (norm_all) xi = Ar::norm(xi);
-            store<W>(x, ld, i, xi);
-            V<W> ri = Ar::add(load<W>(r, ld, i), Ar::mul(nalpha, load_ro<W>(q, ld, i)));
-            if (norm_r) ri = Ar::norm(ri);
-            store<W>(r, ld, i, ri);
-            if (FUSED) acc = Ar::add(acc, Ar::mul(ri, ri));
+        for (int j0 = 0; j0 < TILE_ELEMS; j0 += H) {
+            V<W> xv[H], pv[H], rv[H], qv[H];
+#pragma unroll
+            for (int h2 = 0; h2 < H; h2++) {
+                int64_t i = base + (j0 + h2) * TILE_THREADS;
+                if (i < n) {
+                    xv[h2] = load<W>(x, ld, i);
+                    pv[h2] = load_ro<W>(p, ld, i);
+                    rv[h2] = load<W>(r, ld, i);
+                    qv[h2] = load_ro<W>(q, ld, i);
+                }
+            }
+#pragma unroll
+            for (int h2 = 0; h2 < H; h2++) {
+                int64_t i = base + (j0 + h2) * TILE_THREADS;
+                if (i < n) {
+                    V<W> xi = Ar::add(xv[h2], Ar::mul(alpha, pv[h2]));
+                    if (norm_all) xi = Ar::norm(xi);
+                    store<W>(x, ld, i, xi);
+                    V<W> ri = Ar::add(rv[h2], Ar::mul(nalpha, qv[h2]));
+                    if (norm_r) ri = Ar::norm(ri);
+                    store<W>(r, ld, i, ri);
+                    if (FUSED) acc = Ar::add(acc, Ar::mul(ri, ri));
+                }
+            }
+        }
+        if (FUSED) {
+            acc = block_tree<M, TILE_THREADS>(acc, smem);
+            if (threadIdx.x == 0) store<W>(part, ntiles, tile, acc);
         }
     }
     if (!FUSED) return;
-    acc = block_tree<M, TILE_THREADS>(acc, smem);
-    if (threadIdx.x == 0) store<W>(part, ntiles, blockIdx.x, acc);
     if (!last_block_done(&st->ticket[1], &s_last)) return;
     V<W> rn = reduce_partials_block<M>(part, ntiles, ntiles, smem);
     if (threadIdx.x == 0) {
@@ -196,8 +290,8 @@ __global__ void __launch_bounds__(TILE_THREADS)
 // ---------------------------------------------------------------- K3
 template <int M>
 __global__ void __launch_bounds__(TILE_THREADS)
-    cg_xpay(int64_t n, double *__restrict__ p, const double *__restrict__ r, int64_t ld, CgState *st,
-            cudaGraphConditionalHandle h, int use_cond) {
+    cg_xpay(int64_t n, double *__restrict__ p, const double *__restrict__ r, int64_t ld, int64_t ntiles,
+            CgState *st, cudaGraphConditionalHandle h, int use_cond) {
     using Ar = Arith<M>;
     constexpr int W = Ar::W;
     if (stopped(st, h, use_cond)) return;
@@ -205,14 +299,27 @@ __global__ void __launch_bounds__(TILE_THREADS)
     V<W> beta;
 #pragma unroll
     for (int k = 0; k < W; k++) beta.w[k] = st->beta[k];
-    const int64_t base = (int64_t)blockIdx.x * TILE + threadIdx.x;
+    const int dir = (int)((st->k & 1) ^ 1);
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int64_t tile = snake(t, ntiles, dir);
+        const int64_t base = tile * TILE + threadIdx.x;
+        V<W> rv[TILE_ELEMS], pv[TILE_ELEMS];
 #pragma unroll
-    for (int j = 0; j < TILE_ELEMS; j++) {
-        int64_t i = base + j * TILE_THREADS;
-        if (i < n) {
-            V<W> pi = Ar::add(load_ro<W>(r, ld, i), Ar::mul(beta, load<W>(p, ld, i)));
-            if (norm_all) pi = Ar::norm(pi);
-            store<W>(p, ld, i, pi);
+        for (int j = 0; j < TILE_ELEMS; j++) {
+            int64_t i = base + j * TILE_THREADS;
+            if (i < n) {
+                rv[j] = load_ro<W>(r, ld, i);
+                pv[j] = load<W>(p, ld, i);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < TILE_ELEMS; j++) {
+            int64_t i = base + j * TILE_THREADS;
+            if (i < n) {
+                V<W> pi = Ar::add(rv[j], Ar::mul(beta, pv[j]));
+                if (norm_all) pi = Ar::norm(pi);
+                store<W>(p, ld, i, pi);
+            }
         }
     }
 }
@@ -229,22 +336,26 @@ __global__ void __launch_bounds__(TILE_THREADS)
     __shared__ double smem[W * TILE_THREADS / 32];
     __shared__ int s_last;
     const bool norm_r = st->norm_r != 0;
-    const int64_t base = (int64_t)blockIdx.x * TILE + threadIdx.x;
-    V<W> acc = zero<W>();
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t base = tile * TILE + threadIdx.x;
+        V<W> acc = zero<W>();
 #pragma unroll
-    for (int j = 0; j < TILE_ELEMS; j++) {
-        int64_t i = base + j * TILE_THREADS;
-        if (i < n) {
-            V<W> ri = Ar::dxadd(b[i], neg<W>(load<W>(q, ld, i)));
-            if (norm_r) ri = Ar::norm(ri);
-            store<W>(r, ld, i, ri);
-            store<W>(p, ld, i, ri);
-            if (FUSED) acc = Ar::add(acc, Ar::mul(ri, ri));
+        for (int j = 0; j < TILE_ELEMS; j++) {
+            int64_t i = base + j * TILE_THREADS;
+            if (i < n) {
+                V<W> ri = Ar::dxadd(b[i], neg<W>(load<W>(q, ld, i)));
+                if (norm_r) ri = Ar::norm(ri);
+                store<W>(r, ld, i, ri);
+                store<W>(p, ld, i, ri);
+                if (FUSED) acc = Ar::add(acc, Ar::mul(ri, ri));
+            }
+        }
+        if (FUSED) {
+            acc = block_tree<M, TILE_THREADS>(acc, smem);
+            if (threadIdx.x == 0) store<W>(part, ntiles, tile, acc);
         }
     }
     if (!FUSED) return;
-    acc = block_tree<M, TILE_THREADS>(acc, smem);
-    if (threadIdx.x == 0) store<W>(part, ntiles, blockIdx.x, acc);
     if (!last_block_done(&st->ticket[2], &s_last)) return;
     V<W> rho = reduce_partials_block<M>(part, ntiles, ntiles, smem);
     if (threadIdx.x == 0) {
@@ -360,6 +471,7 @@ struct mwcg_solver {
     cudaGraphExec_t exec = nullptr;
     cudaGraphConditionalHandle cond{};
     cudaEvent_t ev[8] = {};
+    unsigned grid[4] = {1, 1, 1, 1};  // spmv_pq, update, xpay, init
 };
 
 namespace {
@@ -368,23 +480,25 @@ template <int M>
 int enqueue_iteration(mwcg_solver *s, cudaStream_t st, cudaGraphConditionalHandle h, int use_cond) {
     const unsigned tiles = (unsigned)s->ntiles;
     const int64_t ld = s->n;
+    const unsigned g0 = s->grid[0], g1 = s->grid[1], g2 = s->grid[2];
     if (s->fused) {
-        cg_spmv_pq<M, true><<<tiles, TILE_THREADS, 0, st>>>(s->A, s->p, s->q, ld, s->part, s->ntiles,
+        cg_spmv_pq<M, true><<<g0, SpTraits<M>::THREADS, 0, st>>>(s->A, s->p, s->q, ld, s->part, s->ntiles,
                                                              s->st, h, use_cond);
-        cg_update<M, true><<<tiles, TILE_THREADS, 0, st>>>(s->n, s->x, s->r, s->p, s->q, ld, s->part,
-                                                            s->ntiles, s->st, h, use_cond);
+        cg_update<M, true><<<g1, TILE_THREADS, 0, st>>>(s->n, s->x, s->r, s->p, s->q, ld, s->part,
+                                                         s->ntiles, s->st, h, use_cond);
     } else {
         const unsigned pb = (unsigned)((s->parts + 127) / 128);
-        cg_spmv_pq<M, false><<<tiles, TILE_THREADS, 0, st>>>(s->A, s->p, s->q, ld, s->part, s->ntiles,
-                                                              s->st, h, use_cond);
+        cg_spmv_pq<M, false><<<g0, SpTraits<M>::THREADS, 0, st>>>(s->A, s->p, s->q, ld, s->part, s->ntiles,
+                                                           s->st, h, use_cond);
         cg_dot_part<M><<<pb, 128, 0, st>>>(s->n, s->p, s->q, ld, s->parts, s->part, s->st, 1);
         cg_ref_combine<M><<<1, 1, 0, st>>>(s->part, s->parts, s->st, 1, h, use_cond);
-        cg_update<M, false><<<tiles, TILE_THREADS, 0, st>>>(s->n, s->x, s->r, s->p, s->q, ld, s->part,
-                                                             s->ntiles, s->st, h, use_cond);
+        cg_update<M, false><<<g1, TILE_THREADS, 0, st>>>(s->n, s->x, s->r, s->p, s->q, ld, s->part,
+                                                          s->ntiles, s->st, h, use_cond);
         cg_dot_part<M><<<pb, 128, 0, st>>>(s->n, s->r, s->r, ld, s->parts, s->part, s->st, 1);
         cg_ref_combine<M><<<1, 1, 0, st>>>(s->part, s->parts, s->st, 2, h, use_cond);
     }
-    cg_xpay<M><<<tiles, TILE_THREADS, 0, st>>>(s->n, s->p, s->r, ld, s->st, h, use_cond);
+    cg_xpay<M><<<g2, TILE_THREADS, 0, st>>>(s->n, s->p, s->r, ld, s->ntiles, s->st, h, use_cond);
+    (void)tiles;
     MWCG_CHECK_LAUNCH();
     return 0;
 }
@@ -402,7 +516,7 @@ int enqueue_iteration_mode(mwcg_solver *s, cudaStream_t st, cudaGraphConditional
 template <int M>
 int enqueue_init(mwcg_solver *s) {
     cudaStream_t st = s->stream;
-    const unsigned tiles = (unsigned)s->ntiles;
+    const unsigned tiles = s->grid[3];
     if (s->fused) {
         cg_init<M, true><<<tiles, TILE_THREADS, 0, st>>>(s->n, s->b, s->q, s->r, s->p, s->n, s->part,
                                                           s->ntiles, s->st);
@@ -415,6 +529,40 @@ int enqueue_init(mwcg_solver *s) {
     }
     MWCG_CHECK_LAUNCH();
     return 0;
+}
+
+template <int M>
+int compute_grids_t(mwcg_solver *s) {
+    int dev = 0, sms = 0;
+    MWCG_CUDA(cudaGetDevice(&dev));
+    MWCG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    int nb[4] = {1, 1, 1, 1};
+    if (s->fused) {
+        MWCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb[0], cg_spmv_pq<M, true>, SpTraits<M>::THREADS, 0));
+        MWCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb[1], cg_update<M, true>, TILE_THREADS, 0));
+        MWCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb[3], cg_init<M, true>, TILE_THREADS, 0));
+    } else {
+        MWCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb[0], cg_spmv_pq<M, false>, SpTraits<M>::THREADS, 0));
+        MWCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb[1], cg_update<M, false>, TILE_THREADS, 0));
+        MWCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb[3], cg_init<M, false>, TILE_THREADS, 0));
+    }
+    MWCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb[2], cg_xpay<M>, TILE_THREADS, 0));
+    for (int i = 0; i < 4; i++) {
+        int64_t g = (int64_t)(nb[i] > 0 ? nb[i] : 1) * sms;
+        if (g > s->ntiles) g = s->ntiles;
+        s->grid[i] = (unsigned)(g > 0 ? g : 1);
+    }
+    return 0;
+}
+
+int compute_grids(mwcg_solver *s) {
+    switch (s->mode) {
+    case FP64: return compute_grids_t<FP64>(s);
+    case DW: return compute_grids_t<DW>(s);
+    case QDW: return compute_grids_t<QDW>(s);
+    case TW: return compute_grids_t<TW>(s);
+    default: return compute_grids_t<QTW>(s);
+    }
 }
 
 int build_graph(mwcg_solver *s) {
@@ -579,6 +727,11 @@ int mwcg_solver_create(mwcg_solver **out, const mwcg_matrix *A, const mwcg_solve
     for (auto &e : s->ev) TRY(cudaEventCreate(&e));
 #undef TRY
     if (s->n > 0) {
+        rc = compute_grids(s);
+        if (rc) {
+            free_solver(s);
+            return rc;
+        }
         rc = build_graph(s);
         if (rc) {
             free_solver(s);
@@ -669,7 +822,6 @@ int mwcg_solver_run_profiled(mwcg_solver *s, int64_t k_stop, double *ms) {
     MWCG_CUDA(cudaMemcpyAsync(&s->st->k_stop, s->kstop_host, sizeof(long long), cudaMemcpyHostToDevice, st));
     MWCG_CUDA(cudaMemcpyAsync(s->st_host, s->st, sizeof(CgState), cudaMemcpyDeviceToHost, st));
     MWCG_CUDA(cudaStreamSynchronize(st));
-    const unsigned tiles = (unsigned)s->ntiles;
     cudaGraphConditionalHandle h{};
     while (s->st_host->status == RUNNING && s->st_host->k < k_stop) {
         MWCG_CUDA(cudaEventRecord(s->ev[0], st));
@@ -677,26 +829,26 @@ int mwcg_solver_run_profiled(mwcg_solver *s, int64_t k_stop, double *ms) {
     do {                                                                                                   \
         const unsigned pb = (unsigned)((s->parts + 127) / 128);                                            \
         if (s->fused) {                                                                                    \
-            cg_spmv_pq<Mx, true><<<tiles, TILE_THREADS, 0, st>>>(s->A, s->p, s->q, s->n, s->part,          \
+            cg_spmv_pq<Mx, true><<<s->grid[0], SpTraits<Mx>::THREADS, 0, st>>>(s->A, s->p, s->q, s->n, s->part,     \
                                                                   s->ntiles, s->st, h, 0);                 \
         } else {                                                                                           \
-            cg_spmv_pq<Mx, false><<<tiles, TILE_THREADS, 0, st>>>(s->A, s->p, s->q, s->n, s->part,         \
+            cg_spmv_pq<Mx, false><<<s->grid[0], SpTraits<Mx>::THREADS, 0, st>>>(s->A, s->p, s->q, s->n, s->part,    \
                                                                    s->ntiles, s->st, h, 0);                \
             cg_dot_part<Mx><<<pb, 128, 0, st>>>(s->n, s->p, s->q, s->n, s->parts, s->part, s->st, 1);      \
             cg_ref_combine<Mx><<<1, 1, 0, st>>>(s->part, s->parts, s->st, 1, h, 0);                        \
         }                                                                                                  \
         cudaEventRecord(s->ev[1], st);                                                                     \
         if (s->fused) {                                                                                    \
-            cg_update<Mx, true><<<tiles, TILE_THREADS, 0, st>>>(s->n, s->x, s->r, s->p, s->q, s->n,        \
+            cg_update<Mx, true><<<s->grid[1], TILE_THREADS, 0, st>>>(s->n, s->x, s->r, s->p, s->q, s->n,   \
                                                                  s->part, s->ntiles, s->st, h, 0);         \
         } else {                                                                                           \
-            cg_update<Mx, false><<<tiles, TILE_THREADS, 0, st>>>(s->n, s->x, s->r, s->p, s->q, s->n,       \
+            cg_update<Mx, false><<<s->grid[1], TILE_THREADS, 0, st>>>(s->n, s->x, s->r, s->p, s->q, s->n,  \
                                                                   s->part, s->ntiles, s->st, h, 0);        \
             cg_dot_part<Mx><<<pb, 128, 0, st>>>(s->n, s->r, s->r, s->n, s->parts, s->part, s->st, 1);      \
             cg_ref_combine<Mx><<<1, 1, 0, st>>>(s->part, s->parts, s->st, 2, h, 0);                        \
         }                                                                                                  \
         cudaEventRecord(s->ev[2], st);                                                                     \
-        cg_xpay<Mx><<<tiles, TILE_THREADS, 0, st>>>(s->n, s->p, s->r, s->n, s->st, h, 0);                 \
+        cg_xpay<Mx><<<s->grid[2], TILE_THREADS, 0, st>>>(s->n, s->p, s->r, s->n, s->ntiles, s->st, h, 0); \
     } while (0)
         switch (s->mode) {
         case FP64: STAGES(FP64); break;
@@ -824,14 +976,19 @@ int mwcg_cg_solve(mwcg_solver *s, const double *b, double b_norm, const double *
     if (rc) return rc;
     mwcg_state stt{};
     if ((rc = mwcg_solver_state(s, &stt))) return rc;
-    int64_t nh = 0, last_rec = -1;
+    int64_t nh = 0, last_rec = -1, metric_launches = 0;
     double loop_ms = 0.0, hist_ms = 0.0;
     double stage_ms[3] = {0, 0, 0};
     auto record = [&](int64_t k, double rel) -> int {
         double e = NAN, t = NAN;
         cudaEventRecord(s->ev[4], s->stream);
+        const bool first = !s->norms_ready;
         int r2 = mwcg_solver_metrics(s, &e, &t);
         if (r2) return r2;
+        // promote x, metrics rows, 1-2 dots (2 kernels each in partitions mode)
+        const int dk = s->fused ? 1 : 2;
+        metric_launches += 2 + dk * (s->x_star ? 2 : 1);
+        if (first) metric_launches += (1 + dk) * (s->x_star ? 2 : 1);
         cudaEventRecord(s->ev[5], s->stream);
         cudaEventSynchronize(s->ev[5]);
         float ms = 0;
@@ -878,6 +1035,11 @@ int mwcg_cg_solve(mwcg_solver *s, const double *b, double b_norm, const double *
     res->n_hist = nh;
     res->loop_ms = profile ? (stage_ms[0] + stage_ms[1] + stage_ms[2]) : loop_ms;
     res->history_ms = hist_ms;
+    // kernels launched by this solve: SpMV + init, 3 per graph-body run (the
+    // body also runs once for an iteration that breaks down in K1), metrics
+    // (a breakdown is counted as one extra body run: exact for a K1 breakdown)
+    const int64_t bodies = stt.k + (stt.status == BREAKDOWN ? 1 : 0);
+    res->launches = 2 + (s->fused ? 3 : 7) * bodies + metric_launches;
     res->stage_ms[0] = stage_ms[0];
     res->stage_ms[1] = stage_ms[1];
     res->stage_ms[2] = stage_ms[2];

@@ -111,6 +111,57 @@ __device__ __forceinline__ mw::V<mw::Arith<M>::W> block_tree(mw::V<mw::Arith<M>:
     return v;
 }
 
+// Same tree, but only the first NT threads of a (possibly larger) block hold
+// the values; every thread of the block must call it (it synchronises).
+template <int M, int NT>
+__device__ __forceinline__ mw::V<mw::Arith<M>::W> block_tree_first(mw::V<mw::Arith<M>::W> v,
+                                                                   double *smem /* W*NT/32 */) {
+    using A = mw::Arith<M>;
+    constexpr int W = A::W;
+    constexpr int NW = NT / 32;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (wid < NW) {
+        v = warp_tree<M>(v);
+        if (lane == 0) {
+#pragma unroll
+            for (int k = 0; k < W; k++) smem[k * NW + wid] = v.w[k];
+        }
+    }
+    __syncthreads();
+    if (wid == 0) {
+        mw::V<W> u = mw::zero<W>();
+        if (lane < NW) {
+#pragma unroll
+            for (int k = 0; k < W; k++) u.w[k] = smem[k * NW + lane];
+        }
+#pragma unroll
+        for (int off = NW / 2; off >= 1; off >>= 1) {
+            auto o = mw::shfl_down<W>(u, off);
+            u = A::add(u, o);
+        }
+        v = u;
+    }
+    __syncthreads();
+    return v;
+}
+
+template <int M>
+__device__ __forceinline__ mw::V<mw::Arith<M>::W> reduce_partials_first(const double *part, int64_t ld,
+                                                                         int64_t ntiles, double *smem) {
+    using A = mw::Arith<M>;
+    constexpr int W = A::W;
+    mw::V<W> acc = mw::zero<W>();
+    if (threadIdx.x < TILE_THREADS) {
+        for (int64_t idx = threadIdx.x; idx < ntiles; idx += TILE_THREADS) {
+            mw::V<W> t;
+#pragma unroll
+            for (int k = 0; k < W; k++) t.w[k] = __ldcg(part + k * ld + idx);
+            acc = A::add(acc, t);
+        }
+    }
+    return block_tree_first<M, TILE_THREADS>(acc, smem);
+}
+
 // Second pass over ntiles partials (SoA, leading dim ld) by one block of
 // TILE_THREADS threads; identical procedure to a tile with E=ceil(ntiles/TB).
 // Partials written by other CTAs in this grid are read with ld.cg (L2) loads.

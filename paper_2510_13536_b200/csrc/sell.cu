@@ -76,6 +76,9 @@ static int build_sell(SellMatrixOwned *M, const I *rp, const I *ci, const double
     A.total = total;
     MWCG_CUDA(cudaMallocAsync((void **)&M->cols, sizeof(int32_t) * (total > 0 ? total : 1), st));
     MWCG_CUDA(cudaMallocAsync((void **)&M->vals, sizeof(double) * (total > 0 ? total : 1), st));
+    // padding slots: column 0 / value 0, so chunked readers may load them safely
+    MWCG_CUDA(cudaMemsetAsync(M->cols, 0, sizeof(int32_t) * (total > 0 ? total : 1), st));
+    MWCG_CUDA(cudaMemsetAsync(M->vals, 0, sizeof(double) * (total > 0 ? total : 1), st));
     if (A.n_rows > 0) {
         int threads = 256;
         int64_t blocks = (A.n_rows * 32 + threads - 1) / threads;

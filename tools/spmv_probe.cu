@@ -1,0 +1,132 @@
+// spmv_probe.cu -- decomposition microbenchmark for the SELL-32 SpMV on the
+// C2 structure (3-D 7-point, 128^3): where does the time go?
+//   A  coalesced stream of cols+vals only (the matrix bytes)
+//   B  SELL thread-per-row walk, no x gathers (matrix + row_len)
+//   C  B + FP64 x gathers (the full FP64 SpMV without the dot)
+//   D  C with 2 rows per thread interleaved
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o spmv_probe spmv_probe.cu
+#include <cstdio>
+#include <cstdint>
+#include <vector>
+#include <cstdlib>
+#include <cuda_runtime.h>
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s: %s\n", #x, cudaGetErrorString(e)); return 1; } } while (0)
+
+__global__ void stream_kernel(const int4 *__restrict__ c, int64_t nc4, const double2 *__restrict__ v, int64_t nv2, double *out) {
+    double s = 0;
+    int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, st = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = tid; i < nv2; i += st) { double2 a = __ldg(v + i); s += a.x + a.y; }
+    int acc = 0;
+    for (int64_t i = tid; i < nc4; i += st) { int4 a = __ldg(c + i); acc += a.x ^ a.y ^ a.z ^ a.w; }
+    if (s == 1.2345 && acc == 7) out[0] = s;
+}
+
+template <bool GATHER, int RPT>
+__global__ void sell_kernel(const int64_t *__restrict__ sp, const int *__restrict__ rl, const int *__restrict__ cols,
+                            const double *__restrict__ vals, const double *__restrict__ x, double *__restrict__ y, int64_t n) {
+    int64_t r0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
+    int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = r0; base < n; base += stride * RPT) {
+        int len[RPT]; int64_t off[RPT];
+#pragma unroll
+        for (int q = 0; q < RPT; q++) {
+            int64_t row = base + q * stride;
+            len[q] = row < n ? __ldg(rl + row) : 0;
+            off[q] = row < n ? __ldg(sp + (row >> 5)) + (row & 31) : 0;
+        }
+        int c[RPT][8]; double a[RPT][8];
+#pragma unroll
+        for (int q = 0; q < RPT; q++)
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                int kk = min(u, max(len[q] - 1, 0));
+                c[q][u] = __ldg(cols + off[q] + kk * 32);
+                a[q][u] = __ldg(vals + off[q] + kk * 32);
+            }
+#pragma unroll
+        for (int q = 0; q < RPT; q++) {
+            double s = 0;
+            double xv[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) xv[u] = GATHER ? __ldg(x + c[q][u]) : (double)c[q][u];
+#pragma unroll
+            for (int u = 0; u < 8; u++) if (u < len[q]) s = __dadd_rn(s, __dmul_rn(a[q][u], xv[u]));
+            int64_t row = base + q * stride;
+            if (row < n) y[row] = s;
+        }
+    }
+}
+
+int main() {
+    const int k = 128;
+    const int64_t n = (int64_t)k * k * k;
+    // build SELL-32 of the 7-point stencil on the host
+    std::vector<int> rl(n);
+    std::vector<std::vector<int>> rc(n);
+    for (int64_t i = 0; i < n; i++) {
+        int z = i / (k * k), y = (i / k) % k, x = i % k;
+        int64_t cand[7] = {i - k * k, i - k, i - 1, i, i + 1, i + k, i + k * k};
+        bool ok[7] = {z > 0, y > 0, x > 0, true, x < k - 1, y < k - 1, z < k - 1};
+        for (int t = 0; t < 7; t++) if (ok[t]) rc[i].push_back((int)cand[t]);
+        rl[i] = (int)rc[i].size();
+    }
+    int64_t ns = n / 32;
+    std::vector<int64_t> sp(ns + 1, 0);
+    for (int64_t s = 0; s < ns; s++) {
+        int m = 0;
+        for (int l = 0; l < 32; l++) m = std::max(m, rl[s * 32 + l]);
+        sp[s + 1] = sp[s] + (int64_t)m * 32;
+    }
+    int64_t tot = sp[ns];
+    std::vector<int> cols(tot, 0);
+    std::vector<double> vals(tot, 0.0);
+    for (int64_t i = 0; i < n; i++)
+        for (int t = 0; t < rl[i]; t++) {
+            cols[sp[i / 32] + t * 32 + (i % 32)] = rc[i][t];
+            vals[sp[i / 32] + t * 32 + (i % 32)] = t == 3 ? 6.0 : -1.0;
+        }
+    int64_t *d_sp; int *d_rl, *d_c; double *d_v, *d_x, *d_y, *d_o;
+    CK(cudaMalloc(&d_sp, sizeof(int64_t) * (ns + 1))); CK(cudaMalloc(&d_rl, sizeof(int) * n));
+    CK(cudaMalloc(&d_c, sizeof(int) * tot)); CK(cudaMalloc(&d_v, sizeof(double) * tot));
+    CK(cudaMalloc(&d_x, sizeof(double) * n)); CK(cudaMalloc(&d_y, sizeof(double) * n)); CK(cudaMalloc(&d_o, 8));
+    CK(cudaMemcpy(d_sp, sp.data(), sizeof(int64_t) * (ns + 1), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_rl, rl.data(), sizeof(int) * n, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_c, cols.data(), sizeof(int) * tot, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_v, vals.data(), sizeof(double) * tot, cudaMemcpyHostToDevice));
+    CK(cudaMemset(d_x, 0, sizeof(double) * n));
+    // L2 flush buffer
+    double *flush; CK(cudaMalloc(&flush, 512ull << 20)); CK(cudaMemset(flush, 0, 512ull << 20));
+    const bool wflush = getenv("WFLUSH") != nullptr;
+    cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+    int sms = 148;
+    auto timeit = [&](const char *name, double bytes, auto launch) {
+        float best = 1e9;
+        for (int r = 0; r < 6; r++) {
+            if (wflush) cudaMemsetAsync(flush, r, 512ull << 20);
+            else stream_kernel<<<sms * 8, 256>>>((const int4 *)flush, 0, (const double2 *)flush, (512ull << 20) / 16, d_o);
+            cudaEventRecord(e0); launch(); cudaEventRecord(e1); cudaEventSynchronize(e1);
+            float ms; cudaEventElapsedTime(&ms, e0, e1); if (r > 0 && ms < best) best = ms;
+        }
+        printf("%-44s %8.2f us  %7.1f GB/s\n", name, best * 1e3, bytes / (best * 1e-3) / 1e9);
+    };
+    double mbytes = tot * 12.0;
+    for (int bps : {4, 8, 16}) {
+        char nm[64]; snprintf(nm, 64, "A stream cols+vals (blocks/SM=%d)", bps);
+        timeit(nm, mbytes, [&] { stream_kernel<<<sms * bps, 256>>>((const int4 *)d_c, tot / 4, (const double2 *)d_v, tot / 2, d_o); });
+    }
+    double sbytes = mbytes + 4.0 * n + 8.0 * n * 2;
+    for (int bps : {2, 4, 8}) {
+        char nm[64];
+        snprintf(nm, 64, "B sell no-gather rpt1 (blocks/SM=%d)", bps);
+        timeit(nm, sbytes, [&] { sell_kernel<false, 1><<<sms * bps, 256>>>(d_sp, d_rl, d_c, d_v, d_x, d_y, n); });
+        snprintf(nm, 64, "C sell gather rpt1 (blocks/SM=%d)", bps);
+        timeit(nm, sbytes, [&] { sell_kernel<true, 1><<<sms * bps, 256>>>(d_sp, d_rl, d_c, d_v, d_x, d_y, n); });
+        snprintf(nm, 64, "D sell gather rpt2 (blocks/SM=%d)", bps);
+        timeit(nm, sbytes, [&] { sell_kernel<true, 2><<<sms * bps, 256>>>(d_sp, d_rl, d_c, d_v, d_x, d_y, n); });
+    }
+    // one-row-per-thread, full grid (no persistence)
+    timeit("C' sell gather, grid = n/256", sbytes, [&] { sell_kernel<true, 1><<<(unsigned)((n + 255) / 256), 256>>>(d_sp, d_rl, d_c, d_v, d_x, d_y, n); });
+    timeit("B' sell no-gather, grid = n/256", sbytes, [&] { sell_kernel<false, 1><<<(unsigned)((n + 255) / 256), 256>>>(d_sp, d_rl, d_c, d_v, d_x, d_y, n); });
+    return 0;
+}
