@@ -139,14 +139,19 @@ struct SpTraits {
 #ifdef MWCG_SP_THREADS_OVERRIDE
     static constexpr int THREADS = MWCG_SP_THREADS_OVERRIDE;
 #else
-    static constexpr int THREADS = 512;
+    static constexpr int THREADS = (M == TW || M == QTW) ? 256 : 512;
 #endif
 #ifdef MWCG_SP_MINB_OVERRIDE
     static constexpr int MINB = MWCG_SP_MINB_OVERRIDE;
 #else
-    static constexpr int MINB = (M == FP64) ? 3 : 2;
+    static constexpr int MINB = (M == FP64) ? 3 : ((M == TW || M == QTW) ? 4 : 2);
 #endif
     static constexpr int RPT = TILE / THREADS;
+#ifdef MWCG_SP_U_OVERRIDE
+    static constexpr int U = MWCG_SP_U_OVERRIDE;
+#else
+    static constexpr int U = (M == TW || M == QTW) ? 4 : 8;
+#endif
 };
 
 template <int M, bool FUSED>
@@ -173,7 +178,7 @@ __global__ void __launch_bounds__(SpTraits<M>::THREADS, SpTraits<M>::MINB)
             const int64_t row = tile * TILE + li;
             V<W> term = zero<W>();
             if (row < n) {
-                V<W> sv = spmv_row<M, 8>(A, p, ld, row);
+                V<W> sv = spmv_row<M, SpTraits<M>::U>(A, p, ld, row);
                 if (norm_all) sv = Ar::norm(sv);
                 store<W>(q, ld, row, sv);
                 if (FUSED) term = Ar::mul(load_ro<W>(p, ld, row), sv);

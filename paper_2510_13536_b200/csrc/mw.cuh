@@ -120,35 +120,44 @@ MWI V<2> norm_dw(V<2> a) {
 
 // ------------------------------------------------------------ TW / QTW
 // VSEB_m over an error-free chain e[0..N-1] (_fast.py:136-163,
-// multiword.py:187-203): emit rounded partial sums whenever the running
-// error is non-zero; stop after m words.
-template <int N, int M>
+// multiword.py:187-203): emit the rounded partial sum whenever the running
+// error is non-zero; stop after m words.  Branch-free: every step is
+// computed, the emission slot is selected with predicates (cnt <= i is known
+// at compile time per step), and steps after the m-th emission are masked.
+//
+// When e is a VecSum chain (every call site here), step 0 is two_sum(e0, e1)
+// with e1 the exact error of the rounding that produced e0, so
+// fl(e0 + e1) = e0 and the error is e1 for finite e0; for non-finite e0, e1 is
+// NaN and both forms give NaN.  Step 0 therefore costs one DADD
+// (CHAIN = true).
+template <int N, int M, bool CHAIN = true>
 MWI V<3> vseb(const double (&e)[N]) {
     double r0 = 0.0, r1 = 0.0, r2 = 0.0;
-    int j = 0;
+    int cnt = 0;
     bool done = false;
     double eps = e[0];
 #pragma unroll
     for (int i = 0; i < N - 1; i++) {
-        if (!done) {
-            double rj, en;
+        double rj, en;
+        if (CHAIN && i == 0) {
+            rj = __dadd_rn(eps, e[1]);
+            en = e[1];
+        } else {
             two_sum(eps, e[i + 1], rj, en);
-            if (en != 0.0) {
-                if (j == 0) r0 = rj;
-                else if (j == 1) r1 = rj;
-                else r2 = rj;
-                if (j == M - 1) done = true;
-                j++;
-                eps = en;
-            } else {
-                eps = rj;
-            }
         }
+        const bool nz = en != 0.0;
+        const bool emit = nz && !done;
+        r0 = (emit && cnt == 0) ? rj : r0;
+        if (i >= 1) r1 = (emit && cnt == 1) ? rj : r1;
+        if (i >= 2 && M == 3) r2 = (emit && cnt == 2) ? rj : r2;
+        if (i >= M - 1) done = done || (emit && cnt == M - 1);
+        cnt += emit ? 1 : 0;
+        eps = nz ? en : rj;
     }
     if (!done) {
-        if (j == 0) r0 = eps;
-        else if (j == 1) r1 = eps;
-        else r2 = eps;
+        r0 = (cnt == 0) ? eps : r0;
+        r1 = (cnt == 1) ? eps : r1;
+        if (M == 3) r2 = (cnt == 2) ? eps : r2;
     }
     return V<3>{{r0, r1, r2}};
 }
@@ -182,20 +191,40 @@ MWI V<3> renorm3(double c0, double c1, double c2) {
     return vseb<3, 3>(e);
 }
 
-// _tw_add: _fast.py:178-198.  Two-pointer merge by magnitude (not a sort:
-// it reproduces the reference's path exactly, inputs need not be ordered).
+// _tw_add: _fast.py:178-198.  The reference's two-pointer merge by magnitude
+// (ties take the first operand; inputs need not be ordered), written as its
+// state machine: after k steps the state (i, j), i+j = k, is one of at most
+// four predicates, and each output word is a select among the heads that
+// state can see -- no dynamic register indexing.
 MWI V<3> tw_add(V<3> a, V<3> b) {
+    const double a0 = a.w[0], a1 = a.w[1], a2 = a.w[2];
+    const double b0 = b.w[0], b1 = b.w[1], b2 = b.w[2];
+    // head comparisons c_ij = |a_i| >= |b_j|
+    const bool c00 = mag_ge(a0, b0), c10 = mag_ge(a1, b0), c01 = mag_ge(a0, b1);
+    const bool c20 = mag_ge(a2, b0), c11 = mag_ge(a1, b1), c02 = mag_ge(a0, b2);
+    const bool c21 = mag_ge(a2, b1), c12 = mag_ge(a1, b2), c22 = mag_ge(a2, b2);
     double z[6];
-    int i = 0, j = 0;
-#pragma unroll
-    for (int k = 0; k < 6; k++) {
-        double ca = (i == 0) ? a.w[0] : ((i == 1) ? a.w[1] : a.w[2]);
-        double cb = (j == 0) ? b.w[0] : ((j == 1) ? b.w[1] : b.w[2]);
-        bool take_a = (i < 3) && ((j >= 3) || mag_ge(ca, cb));
-        z[k] = take_a ? ca : cb;
-        i += take_a ? 1 : 0;
-        j += take_a ? 0 : 1;
-    }
+    // step 0: state (0,0)
+    z[0] = c00 ? a0 : b0;
+    // step 1: state (1,0) if c00 else (0,1)
+    const bool t1 = c00 ? c10 : c01;  // took from a at step 1
+    z[1] = c00 ? (c10 ? a1 : b0) : (c01 ? a0 : b1);
+    // step 2: states (2,0) (1,1) (0,2)
+    const bool s20 = c00 && t1, s02 = !c00 && !t1, s11 = !s20 && !s02;
+    const bool t2 = s20 ? c20 : (s11 ? c11 : c02);
+    z[2] = s20 ? (c20 ? a2 : b0) : (s11 ? (c11 ? a1 : b1) : (c02 ? a0 : b2));
+    // step 3: states (3,0) (2,1) (1,2) (0,3)
+    const bool s30 = s20 && t2, s21 = (s20 && !t2) || (s11 && t2);
+    const bool s03 = s02 && !t2, s12 = !s30 && !s21 && !s03;
+    const bool t3 = s30 ? false : (s21 ? c21 : (s12 ? c12 : true));
+    z[3] = s30 ? b0 : (s21 ? (c21 ? a2 : b1) : (s12 ? (c12 ? a1 : b2) : a0));
+    // step 4: states (3,1) (2,2) (1,3)
+    const bool s31 = s30 || (s21 && t3), s13 = s03 || (s12 && !t3), s22 = !s31 && !s13;
+    const bool t4 = s31 ? false : (s22 ? c22 : true);
+    z[4] = s31 ? b1 : (s22 ? (c22 ? a2 : b2) : a1);
+    // step 5: states (3,2) (2,3)
+    const bool s32 = s31 || (s22 && t4);
+    z[5] = s32 ? b2 : a2;
     double e[6];
     vec_sum<6>(z, e);
     return vseb<6, 3>(e);
