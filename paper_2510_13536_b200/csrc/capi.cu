@@ -33,6 +33,26 @@ __global__ void fp64_peak_kernel(double *out, int iters, double a, double b) {
     if (s == 12345.678) out[0] = s;  // keep the chains live
 }
 
+cudaError_t pool_alloc(void **p, size_t bytes, cudaStream_t st) {
+    static unsigned configured = 0;  // bit per device
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 32 && !(configured & (1u << dev))) {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        configured |= 1u << dev;
+    }
+    return cudaMallocAsync(p, bytes > 0 ? bytes : 16, st);
+}
+
+void pool_free(void *p, cudaStream_t st) {
+    if (p) cudaFreeAsync(p, st);
+}
+
 }  // namespace mwcg
 
 using namespace mwcg;

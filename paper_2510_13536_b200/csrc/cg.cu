@@ -596,22 +596,21 @@ void free_solver(mwcg_solver *s) {
     if (!s) return;
     if (s->exec) cudaGraphExecDestroy(s->exec);
     if (s->graph) cudaGraphDestroy(s->graph);
-    if (s->own_x) cudaFree(s->x);
-    cudaFree(s->r);
-    cudaFree(s->p);
-    cudaFree(s->q);
-    cudaFree(s->part);
-    cudaFree(s->st);
-    cudaFree(s->xt);
-    cudaFree(s->res);
-    cudaFree(s->diff);
-    cudaFree(s->bt);
-    cudaFree(s->mpart);
-    cudaFree(s->mout);
-    cudaFree(s->mticket);
+    cudaStream_t st = s->stream;
+    if (s->own_x) pool_free(s->x, st);
+    pool_free(s->r, st);
+    pool_free(s->p, st);
+    pool_free(s->q, st);
+    pool_free(s->part, st);
+    pool_free(s->st, st);
+    pool_free(s->xt, st);
+    pool_free(s->res, st);
+    pool_free(s->diff, st);
+    pool_free(s->bt, st);
+    pool_free(s->mpart, st);
+    pool_free(s->mout, st);
+    pool_free(s->mticket, st);
     if (s->st_host) cudaFreeHost(s->st_host);
-    if (s->kstop_host) cudaFreeHost(s->kstop_host);
-    if (s->mout_host) cudaFreeHost(s->mout_host);
     for (auto &e : s->ev)
         if (e) cudaEventDestroy(e);
     if (s->cap) cudaStreamDestroy(s->cap);
@@ -715,19 +714,20 @@ int mwcg_solver_create(mwcg_solver **out, const mwcg_matrix *A, const mwcg_solve
     if (x) {
         s->x = x;
     } else {
-        TRY(cudaMalloc(&s->x, vbytes));
+        TRY(pool_alloc((void **)&s->x, vbytes, s->stream));
         s->own_x = true;
     }
-    TRY(cudaMalloc(&s->r, vbytes));
-    TRY(cudaMalloc(&s->p, vbytes));
-    TRY(cudaMalloc(&s->q, vbytes));
+    TRY(pool_alloc((void **)&s->r, vbytes, s->stream));
+    TRY(pool_alloc((void **)&s->p, vbytes, s->stream));
+    TRY(pool_alloc((void **)&s->q, vbytes, s->stream));
     int64_t np = s->fused ? (s->ntiles > 0 ? s->ntiles : 1) : s->parts;
-    TRY(cudaMalloc(&s->part, sizeof(double) * 3 * (size_t)np));
-    TRY(cudaMalloc(&s->st, sizeof(CgState)));
-    TRY(cudaMemset(s->st, 0, sizeof(CgState)));
-    TRY(cudaMallocHost(&s->st_host, sizeof(CgState)));
-    TRY(cudaMallocHost(&s->kstop_host, sizeof(long long)));
-    TRY(cudaMallocHost(&s->mout_host, sizeof(double) * 12));
+    TRY(pool_alloc((void **)&s->part, sizeof(double) * 3 * (size_t)np, s->stream));
+    TRY(pool_alloc((void **)&s->st, sizeof(CgState), s->stream));
+    TRY(cudaMemsetAsync(s->st, 0, sizeof(CgState), s->stream));
+    // one pinned block for the host mirrors: state, k_stop, metric sums
+    TRY(cudaMallocHost((void **)&s->st_host, sizeof(CgState) + 16 * sizeof(double)));
+    s->kstop_host = (long long *)((char *)s->st_host + sizeof(CgState));
+    s->mout_host = (double *)((char *)s->st_host + sizeof(CgState) + 2 * sizeof(double));
     TRY(cudaStreamCreateWithFlags(&s->cap, cudaStreamNonBlocking));
     for (auto &e : s->ev) TRY(cudaEventCreate(&e));
 #undef TRY
@@ -916,14 +916,14 @@ int mwcg_solver_metrics(mwcg_solver *s, double *err, double *true_res) {
     }
     const size_t b3 = sizeof(double) * 3 * (size_t)n;
     if (!s->xt) {
-        MWCG_CUDA(cudaMalloc(&s->xt, b3));
-        MWCG_CUDA(cudaMalloc(&s->res, b3));
-        MWCG_CUDA(cudaMalloc(&s->diff, b3));
-        MWCG_CUDA(cudaMalloc(&s->bt, b3));
-        MWCG_CUDA(cudaMalloc(&s->mpart, sizeof(double) * 3 * (size_t)(s->ntiles > 0 ? s->ntiles : 1)));
-        MWCG_CUDA(cudaMalloc(&s->mout, sizeof(double) * 12));
-        MWCG_CUDA(cudaMalloc(&s->mticket, sizeof(unsigned int)));
-        MWCG_CUDA(cudaMemset(s->mticket, 0, sizeof(unsigned int)));
+        MWCG_CUDA(pool_alloc((void **)&s->xt, b3, st));
+        MWCG_CUDA(pool_alloc((void **)&s->res, b3, st));
+        MWCG_CUDA(pool_alloc((void **)&s->diff, b3, st));
+        MWCG_CUDA(pool_alloc((void **)&s->bt, b3, st));
+        MWCG_CUDA(pool_alloc((void **)&s->mpart, sizeof(double) * 3 * (size_t)(s->ntiles > 0 ? s->ntiles : 1), st));
+        MWCG_CUDA(pool_alloc((void **)&s->mout, sizeof(double) * 12, st));
+        MWCG_CUDA(pool_alloc((void **)&s->mticket, sizeof(unsigned int), st));
+        MWCG_CUDA(cudaMemsetAsync(s->mticket, 0, sizeof(unsigned int), st));
     }
     const unsigned eb = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16);
     int rc;

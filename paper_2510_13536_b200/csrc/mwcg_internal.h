@@ -42,4 +42,10 @@ int launch_scalar_op(int op, int mode, const double *a, const double *b, double 
 
 inline bool valid_mode(int m) { return m >= 0 && m <= 4; }
 
+// Device memory comes from the stream-ordered pool (cudaMallocAsync) with the
+// release threshold raised, so repeated solves / matrix rebuilds reuse memory
+// instead of paying cudaMalloc/cudaFree (capi.cu).
+cudaError_t pool_alloc(void **p, size_t bytes, cudaStream_t st);
+void pool_free(void *p, cudaStream_t st);
+
 }  // namespace mwcg

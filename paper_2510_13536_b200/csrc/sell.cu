@@ -51,9 +51,9 @@ static int build_sell(SellMatrixOwned *M, const I *rp, const I *ci, const double
     SellMatrix &A = M->view;
     int64_t n_pad = A.n_slices * SLICE;
     int64_t *slice_sz = nullptr;
-    MWCG_CUDA(cudaMallocAsync((void **)&M->row_len, sizeof(int32_t) * (n_pad > 0 ? n_pad : 1), st));
-    MWCG_CUDA(cudaMallocAsync((void **)&M->slice_ptr, sizeof(int64_t) * (A.n_slices + 1), st));
-    MWCG_CUDA(cudaMallocAsync((void **)&slice_sz, sizeof(int64_t) * (A.n_slices + 1), st));
+    MWCG_CUDA(pool_alloc((void **)&M->row_len, sizeof(int32_t) * (n_pad > 0 ? n_pad : 1), st));
+    MWCG_CUDA(pool_alloc((void **)&M->slice_ptr, sizeof(int64_t) * (A.n_slices + 1), st));
+    MWCG_CUDA(pool_alloc((void **)&slice_sz, sizeof(int64_t) * (A.n_slices + 1), st));
     MWCG_CUDA(cudaMemsetAsync(slice_sz, 0, sizeof(int64_t) * (A.n_slices + 1), st));
     if (n_pad > 0) {
         int threads = 256;
@@ -65,17 +65,17 @@ static int build_sell(SellMatrixOwned *M, const I *rp, const I *ci, const double
     size_t tmp_bytes = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, slice_sz, M->slice_ptr, A.n_slices + 1, st);
     void *tmp = nullptr;
-    MWCG_CUDA(cudaMallocAsync(&tmp, tmp_bytes, st));
+    MWCG_CUDA(pool_alloc(&tmp, tmp_bytes, st));
     MWCG_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, slice_sz, M->slice_ptr, A.n_slices + 1, st));
     int64_t total = 0;
     MWCG_CUDA(cudaMemcpyAsync(&total, M->slice_ptr + A.n_slices, sizeof(int64_t),
                               cudaMemcpyDeviceToHost, st));
     MWCG_CUDA(cudaStreamSynchronize(st));
-    MWCG_CUDA(cudaFreeAsync(tmp, st));
-    MWCG_CUDA(cudaFreeAsync(slice_sz, st));
+    pool_free(tmp, st);
+    pool_free(slice_sz, st);
     A.total = total;
-    MWCG_CUDA(cudaMallocAsync((void **)&M->cols, sizeof(int32_t) * (total > 0 ? total : 1), st));
-    MWCG_CUDA(cudaMallocAsync((void **)&M->vals, sizeof(double) * (total > 0 ? total : 1), st));
+    MWCG_CUDA(pool_alloc((void **)&M->cols, sizeof(int32_t) * (total > 0 ? total : 1), st));
+    MWCG_CUDA(pool_alloc((void **)&M->vals, sizeof(double) * (total > 0 ? total : 1), st));
     // padding slots: column 0 / value 0, so chunked readers may load them safely
     MWCG_CUDA(cudaMemsetAsync(M->cols, 0, sizeof(int32_t) * (total > 0 ? total : 1), st));
     MWCG_CUDA(cudaMemsetAsync(M->vals, 0, sizeof(double) * (total > 0 ? total : 1), st));
@@ -127,10 +127,10 @@ int sell_create(SellMatrixOwned **out, int64_t n_rows, int64_t n_cols, int64_t n
 
 void sell_destroy(SellMatrixOwned *M) {
     if (!M) return;
-    cudaFree(M->row_len);
-    cudaFree(M->slice_ptr);
-    cudaFree(M->cols);
-    cudaFree(M->vals);
+    pool_free(M->row_len, 0);
+    pool_free(M->slice_ptr, 0);
+    pool_free(M->cols, 0);
+    pool_free(M->vals, 0);
     delete M;
 }
 
