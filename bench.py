@@ -55,6 +55,10 @@ def parse():
     ap.add_argument("--no-per-arith", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--partitioned", action="store_true",
+                    help="force the row-partitioned NCCL path (also at N=1 under torchrun)")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N>1: independent replicas instead of the row-partitioned solver")
     return ap.parse_args()
 
 
@@ -205,7 +209,7 @@ def run_ours(a):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1:
+    if world > 1 or a.partitioned:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2510_13536_b200 import cg, kernels, _lib
     from paper_2510_13536_b200.cg import Solver, _b_norm
@@ -229,6 +233,8 @@ def run_ours(a):
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return float(t.item())
 
+    if (world > 1 and not a.replicas) or a.partitioned:
+        return run_partitioned(a, world, rank, local, dist, torch)
     cfg = load_problem(a.config)
     A, b, xs = cfg["A"], cfg["b"], cfg["x_star"]
     n, nnz, mode = A.n_rows, A.nnz, a.mode
@@ -406,6 +412,72 @@ def run_ours(a):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+    return 0
+
+
+def run_partitioned(a, world, rank, local, dist, torch):
+    """Row-partitioned CG over NCCL, weak scaling: the C2
+    Poisson grid grows along z with N (128 x 128 x 128N), each rank owns
+    ~2.1M rows.  value = C2-equivalent CG iterations/s =
+    (global rows x iterations / s) / n(C2), which equals plain iterations/s
+    at N=1."""
+    from paper_2510_13536_b200 import problems
+    from paper_2510_13536_b200.cg import _b_norm
+    from paper_2510_13536_b200.dist import (RankSolver, TorchDistExchange, dist_cg_solve,
+                                            local_rows, partition)
+    mode = a.mode
+    A = problems.stencil_matrix((128 * world, 128, 128),
+                                [(-1, 0, 0), (0, -1, 0), (0, 0, -1), (0, 0, 1), (0, 1, 0), (1, 0, 0)],
+                                6.0)
+    n = A.n_rows
+    b = problems.spmv_fp64_host(A, np.ones(n))
+    bn = _b_norm(b)
+    part = partition(n, world)
+    lo, hi = part.rows(rank)
+    rs = RankSolver(local_rows(A, lo, hi), part, rank, mode)
+    b_loc = torch.from_numpy(np.ascontiguousarray(b[lo:hi])).cuda()
+    ex = TorchDistExchange()
+    eps, max_it = 1e-12, 20000
+
+    def solve():
+        rs.start(b_loc, bn, None, eps, max_it)
+        return dist_cg_solve([rs], ex, bn, eps, max_it, check_every=32)
+
+    for _ in range(max(1, a.warmup)):
+        solve()
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record()
+        its = 0
+        for _ in range(a.steps):
+            its += solve().iterations
+        e1.record()
+        torch.cuda.synchronize()
+    dt = e0.elapsed_time(e1) * 1e-3
+    t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dt = float(t.item())
+    n_c2 = 128 ** 3
+    value = n * its / dt / n_c2
+    if rank == 0:
+        line = {
+            "metric": "CG iterations/s", "value": value, "unit": "iter/s (C2-equivalent)",
+            "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": 1e3 * dt / a.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"3-D 7-point Poisson 128x128x{128 * world} (C2 per GPU), CG in "
+                                   f"{mode.upper()} to 1e-12, row-partitioned",
+                       "n": n, "nnz": A.nnz, "mode": mode,
+                       "iterations_per_solve": its // a.steps,
+                       "parallelism": f"row partition over {world} GPUs: NCCL all-gather of p "
+                                      "+ tile-partial all-gather, canonical reduction",
+                       "value_definition": "global rows x iterations / s / 128^3"},
+            "gpu_launches": None, "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
     return 0
 
 

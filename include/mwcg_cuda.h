@@ -147,6 +147,26 @@ int mwcg_cg_solve(mwcg_solver *s, const double *b, double b_norm, const double *
                   int64_t history_stride, int profile, mwcg_solve_result *res,
                   int64_t hist_cap, int64_t *h_k, double *h_rel, double *h_true, double *h_err);
 
+/* ---- row-partitioned multi-GPU rank (driven by dist.py) ----
+ * A: this rank's rows, GLOBAL column indices.  p_full (w x ldp) and part
+ * (w x part_ld) are caller-owned; the caller all-gathers p_full after XPAY
+ * and the tile partials before each FINAL stage.  x0 for mwcg_solver_start
+ * is the full (ldp) initial guess.  Results are bitwise identical to the
+ * 1-GPU tile-order solve. */
+enum {
+    MWCG_STAGE_INIT = 0,        /* r = b - q, p = r, r.r partials (after start's SpMV) */
+    MWCG_STAGE_FINAL_INIT = 1,  /* canonical reduce of all partials: rho, rel, stop-at-0 */
+    MWCG_STAGE_SPMV = 2,        /* q = A p, p.q partials */
+    MWCG_STAGE_FINAL_ALPHA = 3, /* reduce, breakdown test, alpha */
+    MWCG_STAGE_UPDATE = 4,      /* x, r update, r.r partials */
+    MWCG_STAGE_FINAL_BETA = 5,  /* reduce, rel, stop / breakdown, beta, k++ */
+    MWCG_STAGE_XPAY = 6         /* p slice = r + beta p */
+};
+int mwcg_solver_create_dist(mwcg_solver **out, const mwcg_matrix *A, const mwcg_solver_config *cfg,
+                            double *x, double *p_full, int64_t ldp, int64_t p_off, double *part,
+                            int64_t part_ld, int64_t tile_off, int64_t ntiles_glob, void *stream);
+int mwcg_solver_dist_stage(mwcg_solver *s, int stage);
+
 /* ---- measurement helpers (bench.py) ---- */
 /* FP64 pipe microbenchmark: DFMA chains on all SMs; returns FP64 ops/s
  * (FMA = 1 op, the SURVEY §8(d) convention) and the elapsed ms. */

@@ -514,6 +514,29 @@ static mw tile_tree_dot_impl(int mode, int64_t n, const double *x, const double 
     return r;
 }
 
+/* Per-tile partials of the canonical tile tree (the first pass of
+ * tile_tree_dot_impl) written SoA into out[k*ld + tile_off + b]. */
+void orc_tile_partials(int mode, int64_t n, const double *x, int64_t ldx, const double *y,
+                       int64_t ldy, int tb, int e, double *out, int64_t ldo, int64_t tile_off) {
+    int w = WORDS[mode];
+    int64_t T = (int64_t)tb * e;
+    int64_t ntiles = (n + T - 1) / T;
+    mw *acc = (mw *)malloc(sizeof(mw) * (size_t)tb);
+    for (int64_t b = 0; b < ntiles; b++) {
+        for (int t = 0; t < tb; t++) {
+            mw a = {{0.0, 0.0, 0.0}};
+            for (int j = 0; j < e; j++) {
+                int64_t i = b * T + (int64_t)j * tb + t;
+                if (i < n) a = op_add(mode, a, op_mul(mode, ld(x, ldx, w, i), ld(y, ldy, w, i)));
+            }
+            acc[t] = a;
+        }
+        mw r = tree_combine(mode, acc, tb);
+        st(out + tile_off, ldo, w, b, r);
+    }
+    free(acc);
+}
+
 void orc_dot_tile(int mode, int64_t n, const double *x, const double *y, int tb, int e,
                   double *out) {
     mw r = tile_tree_dot_impl(mode, n, x, y, tb, e);

@@ -135,6 +135,17 @@ def dot(mode, x, y, partitions=1, tile=None):
     return out[:WORDS[mode]]
 
 
+def tile_partials(mode, x, y, out, tile_off):
+    """Canonical per-tile partials of x.y written into out[:, tile_off:...]
+    (out: (w, ld) float64, C-contiguous)."""
+    x, y = _soa(x, mode), _soa(y, mode)
+    assert out.flags.c_contiguous and out.dtype == np.float64
+    lib().orc_tile_partials(MODE_ID[mode], ctypes.c_int64(x.shape[1]), _p(x),
+                            ctypes.c_int64(x.shape[1]), _p(y), ctypes.c_int64(y.shape[1]),
+                            TILE_THREADS, TILE_ELEMS, _p(out), ctypes.c_int64(out.shape[1]),
+                            ctypes.c_int64(tile_off))
+
+
 def reduce_partials(mode, parts):
     parts = _soa(parts, mode)
     out = np.zeros(3)

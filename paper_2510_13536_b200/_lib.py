@@ -15,6 +15,8 @@ WORDS = {"fp64": 1, "dw": 2, "qdw": 2, "tw": 3, "qtw": 3}
 NORM_ID = {"none": 0, "after-axpy": 1, "every-op": 2}
 RED_ID = {"tile": 0, "partitions": 1}
 STATUS = {0: "running", 1: "converged", 2: "max_iterations", 3: "breakdown"}
+STAGE = {"init": 0, "final_init": 1, "spmv": 2, "final_alpha": 3, "update": 4, "final_beta": 5,
+         "xpay": 6}
 ERR_VALUE = 1001
 
 c_i64 = ctypes.c_int64
@@ -76,6 +78,10 @@ SIGNATURES = {
                                      c_i64, c_i64, ctypes.c_int, ctypes.POINTER(SolveResultC),
                                      c_i64, ctypes.POINTER(c_i64), c_dp, c_dp, c_dp]),
     "mwcg_fp64_peak": (ctypes.c_int, [c_dp, c_dp, c_vp]),
+    "mwcg_solver_create_dist": (ctypes.c_int, [ctypes.POINTER(c_vp), c_vp,
+                                               ctypes.POINTER(SolverConfigC), c_vp, c_vp, c_i64,
+                                               c_i64, c_vp, c_i64, c_i64, c_i64, c_vp]),
+    "mwcg_solver_dist_stage": (ctypes.c_int, [c_vp, ctypes.c_int]),
 }
 
 _lib = None

@@ -122,6 +122,17 @@ __device__ __forceinline__ int64_t snake(int64_t t, int64_t ntiles, int dir) {
     return dir ? (ntiles - 1 - t) : t;
 }
 
+// Geometry of one solver's rows.  Single GPU: n = ld = ldp = n_rows, p_off =
+// tile_off = 0, part_ld = ntiles = ntiles_glob, final_ = 1.  Rank r of a row
+// partition: local rows / tiles, p a full replica (ldp =
+// padded global length) with the local slice at p_off, partials written at
+// global tile indices, final_ = 0 (reduced by cg_finalize after the gather).
+struct Geo {
+    int64_t n, ld, ldp, p_off;
+    int64_t ntiles, tile_off, part_ld, ntiles_glob;
+    int final_;
+};
+
 // Persistent tile loop: every fused kernel runs grid = min(ntiles, resident
 // CTAs) blocks, block b handling tiles b, b+grid, ...  Partials are indexed by
 // tile, so the reduction order is independent of the grid size.
@@ -156,9 +167,8 @@ struct SpTraits {
 
 template <int M, bool FUSED>
 __global__ void __launch_bounds__(SpTraits<M>::THREADS, SpTraits<M>::MINB)
-    cg_spmv_pq(SellMatrix A, const double *__restrict__ p, double *__restrict__ q, int64_t ld,
-               double *__restrict__ part, int64_t ntiles, CgState *st, cudaGraphConditionalHandle h,
-               int use_cond) {
+    cg_spmv_pq(SellMatrix A, const double *__restrict__ p, double *__restrict__ q, Geo g,
+               double *__restrict__ part, CgState *st, cudaGraphConditionalHandle h, int use_cond) {
     using Ar = Arith<M>;
     constexpr int W = Ar::W;
     constexpr int NT = SpTraits<M>::THREADS;
@@ -168,20 +178,21 @@ __global__ void __launch_bounds__(SpTraits<M>::THREADS, SpTraits<M>::MINB)
     __shared__ int s_last;
     if (stopped(st, h, use_cond)) return;
     const bool norm_all = st->norm_all != 0;
-    const int64_t n = A.n_rows;
+    const int64_t n = g.n;
     const int dir = (int)(st->k & 1);
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const int64_t tile = snake(t, ntiles, dir);
+    for (int64_t t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
+        const int64_t tile = snake(t, g.ntiles, dir);
 #pragma unroll 1
         for (int k = 0; k < RPT; k++) {
             const int li = threadIdx.x + k * NT;  // row inside the tile
             const int64_t row = tile * TILE + li;
             V<W> term = zero<W>();
             if (row < n) {
-                V<W> sv = spmv_row<M, SpTraits<M>::U>(A, p, ld, row);
+                // columns are global: p is the full (replicated) vector
+                V<W> sv = spmv_row<M, SpTraits<M>::U>(A, p, g.ldp, row);
                 if (norm_all) sv = Ar::norm(sv);
-                store<W>(q, ld, row, sv);
-                if (FUSED) term = Ar::mul(load_ro<W>(p, ld, row), sv);
+                store<W>(q, g.ld, row, sv);
+                if (FUSED) term = Ar::mul(load_ro<W>(p, g.ldp, g.p_off + row), sv);
             }
             if (FUSED) {
 #pragma unroll
@@ -204,12 +215,12 @@ __global__ void __launch_bounds__(SpTraits<M>::THREADS, SpTraits<M>::MINB)
                 }
             }
             acc = block_tree_first<M, TILE_THREADS>(acc, smem);
-            if (threadIdx.x == 0) store<W>(part, ntiles, tile, acc);
+            if (threadIdx.x == 0) store<W>(part, g.part_ld, g.tile_off + tile, acc);
         }
     }
-    if (!FUSED) return;
+    if (!FUSED || !g.final_) return;
     if (!last_block_done(&st->ticket[0], &s_last)) return;
-    V<W> pq = reduce_partials_first<M>(part, ntiles, ntiles, smem);
+    V<W> pq = reduce_partials_first<M>(part, g.part_ld, g.ntiles_glob, smem);
     if (threadIdx.x == 0) {
         st->ticket[0] = 0u;
         scalar_alpha<M>(st, pq, h, use_cond);
@@ -217,8 +228,6 @@ __global__ void __launch_bounds__(SpTraits<M>::THREADS, SpTraits<M>::MINB)
 }
 
 // ---------------------------------------------------------------- K2
-// All loads of a tile are issued before any arithmetic (the compiler will not
-// hoist loads of x/r above the stores of the previous element by itself).
 // Loads are hoisted HOIST elements at a time (all loads of a group issue
 // before any arithmetic; the compiler does not hoist loads of x/r above the
 // stores of the previous element by itself).  TW is FP64-bound: no hoisting,
@@ -230,9 +239,9 @@ struct Hoist {
 
 template <int M, bool FUSED>
 __global__ void __launch_bounds__(TILE_THREADS)
-    cg_update(int64_t n, double *__restrict__ x, double *__restrict__ r, const double *__restrict__ p,
-              const double *__restrict__ q, int64_t ld, double *__restrict__ part, int64_t ntiles,
-              CgState *st, cudaGraphConditionalHandle h, int use_cond) {
+    cg_update(double *__restrict__ x, double *__restrict__ r, const double *__restrict__ p,
+              const double *__restrict__ q, Geo g, double *__restrict__ part, CgState *st,
+              cudaGraphConditionalHandle h, int use_cond) {
     using Ar = Arith<M>;
     constexpr int W = Ar::W;
     constexpr int H = Hoist<M>::value;
@@ -246,9 +255,11 @@ __global__ void __launch_bounds__(TILE_THREADS)
         alpha.w[k] = st->alpha[k];
         nalpha.w[k] = st->neg_alpha[k];
     }
+    const int64_t n = g.n, ld = g.ld, ldp = g.ldp;
+    const double *__restrict__ pl = p + g.p_off;  // local slice of p
     const int dir = (int)((st->k & 1) ^ 1);
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const int64_t tile = snake(t, ntiles, dir);
+    for (int64_t t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
+        const int64_t tile = snake(t, g.ntiles, dir);
         const int64_t base = tile * TILE + threadIdx.x;
         V<W> acc = zero<W>();
 #pragma unroll
@@ -259,7 +270,7 @@ __global__ void __launch_bounds__(TILE_THREADS)
                 int64_t i = base + (j0 + h2) * TILE_THREADS;
                 if (i < n) {
                     xv[h2] = load<W>(x, ld, i);
-                    pv[h2] = load_ro<W>(p, ld, i);
+                    pv[h2] = load_ro<W>(pl, ldp, i);
                     rv[h2] = load<W>(r, ld, i);
                     qv[h2] = load_ro<W>(q, ld, i);
                 }
@@ -280,12 +291,12 @@ __global__ void __launch_bounds__(TILE_THREADS)
         }
         if (FUSED) {
             acc = block_tree<M, TILE_THREADS>(acc, smem);
-            if (threadIdx.x == 0) store<W>(part, ntiles, tile, acc);
+            if (threadIdx.x == 0) store<W>(part, g.part_ld, g.tile_off + tile, acc);
         }
     }
-    if (!FUSED) return;
+    if (!FUSED || !g.final_) return;
     if (!last_block_done(&st->ticket[1], &s_last)) return;
-    V<W> rn = reduce_partials_block<M>(part, ntiles, ntiles, smem);
+    V<W> rn = reduce_partials_block<M>(part, g.part_ld, g.ntiles_glob, smem);
     if (threadIdx.x == 0) {
         st->ticket[1] = 0u;
         scalar_beta<M>(st, rn, h, use_cond);
@@ -295,8 +306,8 @@ __global__ void __launch_bounds__(TILE_THREADS)
 // ---------------------------------------------------------------- K3
 template <int M>
 __global__ void __launch_bounds__(TILE_THREADS)
-    cg_xpay(int64_t n, double *__restrict__ p, const double *__restrict__ r, int64_t ld, int64_t ntiles,
-            CgState *st, cudaGraphConditionalHandle h, int use_cond) {
+    cg_xpay(double *__restrict__ p, const double *__restrict__ r, Geo g, CgState *st,
+            cudaGraphConditionalHandle h, int use_cond) {
     using Ar = Arith<M>;
     constexpr int W = Ar::W;
     if (stopped(st, h, use_cond)) return;
@@ -304,9 +315,11 @@ __global__ void __launch_bounds__(TILE_THREADS)
     V<W> beta;
 #pragma unroll
     for (int k = 0; k < W; k++) beta.w[k] = st->beta[k];
+    const int64_t n = g.n, ld = g.ld, ldp = g.ldp;
+    double *__restrict__ pl = p + g.p_off;
     const int dir = (int)((st->k & 1) ^ 1);
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const int64_t tile = snake(t, ntiles, dir);
+    for (int64_t t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
+        const int64_t tile = snake(t, g.ntiles, dir);
         const int64_t base = tile * TILE + threadIdx.x;
         V<W> rv[TILE_ELEMS], pv[TILE_ELEMS];
 #pragma unroll
@@ -314,7 +327,7 @@ __global__ void __launch_bounds__(TILE_THREADS)
             int64_t i = base + j * TILE_THREADS;
             if (i < n) {
                 rv[j] = load_ro<W>(r, ld, i);
-                pv[j] = load<W>(p, ld, i);
+                pv[j] = load<W>(pl, ldp, i);
             }
         }
 #pragma unroll
@@ -323,7 +336,7 @@ __global__ void __launch_bounds__(TILE_THREADS)
             if (i < n) {
                 V<W> pi = Ar::add(rv[j], Ar::mul(beta, pv[j]));
                 if (norm_all) pi = Ar::norm(pi);
-                store<W>(p, ld, i, pi);
+                store<W>(pl, ldp, i, pi);
             }
         }
     }
@@ -334,14 +347,16 @@ __global__ void __launch_bounds__(TILE_THREADS)
 // rho = r.r (118), rel, converged-at-0 test (147-148).
 template <int M, bool FUSED>
 __global__ void __launch_bounds__(TILE_THREADS)
-    cg_init(int64_t n, const double *__restrict__ b, const double *__restrict__ q, double *__restrict__ r,
-            double *__restrict__ p, int64_t ld, double *__restrict__ part, int64_t ntiles, CgState *st) {
+    cg_init(const double *__restrict__ b, const double *__restrict__ q, double *__restrict__ r,
+            double *__restrict__ p, Geo g, double *__restrict__ part, CgState *st) {
     using Ar = Arith<M>;
     constexpr int W = Ar::W;
     __shared__ double smem[W * TILE_THREADS / 32];
     __shared__ int s_last;
     const bool norm_r = st->norm_r != 0;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t n = g.n, ld = g.ld, ldp = g.ldp;
+    double *__restrict__ pl = p + g.p_off;
+    for (int64_t tile = blockIdx.x; tile < g.ntiles; tile += gridDim.x) {
         const int64_t base = tile * TILE + threadIdx.x;
         V<W> acc = zero<W>();
 #pragma unroll
@@ -351,21 +366,42 @@ __global__ void __launch_bounds__(TILE_THREADS)
                 V<W> ri = Ar::dxadd(b[i], neg<W>(load<W>(q, ld, i)));
                 if (norm_r) ri = Ar::norm(ri);
                 store<W>(r, ld, i, ri);
-                store<W>(p, ld, i, ri);
+                store<W>(pl, ldp, i, ri);
                 if (FUSED) acc = Ar::add(acc, Ar::mul(ri, ri));
             }
         }
         if (FUSED) {
             acc = block_tree<M, TILE_THREADS>(acc, smem);
-            if (threadIdx.x == 0) store<W>(part, ntiles, tile, acc);
+            if (threadIdx.x == 0) store<W>(part, g.part_ld, g.tile_off + tile, acc);
         }
     }
-    if (!FUSED) return;
+    if (!FUSED || !g.final_) return;
     if (!last_block_done(&st->ticket[2], &s_last)) return;
-    V<W> rho = reduce_partials_block<M>(part, ntiles, ntiles, smem);
+    V<W> rho = reduce_partials_block<M>(part, g.part_ld, g.ntiles_glob, smem);
     if (threadIdx.x == 0) {
         st->ticket[2] = 0u;
         scalar_init<M>(st, rho);
+    }
+}
+
+// ---------------------------------------------------------------- finalize (multi-rank)
+// After the tile partials of every rank have been gathered, one block reduces
+// all global tiles in the canonical order and runs the scalar step -- the
+// same procedure as the fused last-block path, so R ranks reproduce the
+// 1-GPU result bit for bit.  phase 0: init (rho), 1: alpha (p.q), 2: beta.
+template <int M>
+__global__ void __launch_bounds__(TILE_THREADS)
+    cg_finalize(const double *__restrict__ part, Geo g, CgState *st, int phase) {
+    using Ar = Arith<M>;
+    constexpr int W = Ar::W;
+    __shared__ double smem[W * TILE_THREADS / 32];
+    if (phase != 0 && st->status != RUNNING) return;
+    V<W> v = reduce_partials_block<M>(part, g.part_ld, g.ntiles_glob, smem);
+    if (threadIdx.x == 0) {
+        cudaGraphConditionalHandle h{};
+        if (phase == 0) scalar_init<M>(st, v);
+        else if (phase == 1) scalar_alpha<M>(st, v, h, 0);
+        else scalar_beta<M>(st, v, h, 0);
     }
 }
 
@@ -477,33 +513,33 @@ struct mwcg_solver {
     cudaGraphConditionalHandle cond{};
     cudaEvent_t ev[8] = {};
     unsigned grid[4] = {1, 1, 1, 1};  // spmv_pq, update, xpay, init
+    Geo geo{};
+    bool dist = false;                   // rank of a row partition (no graph; see dist.py)
 };
 
 namespace {
 
 template <int M>
 int enqueue_iteration(mwcg_solver *s, cudaStream_t st, cudaGraphConditionalHandle h, int use_cond) {
-    const unsigned tiles = (unsigned)s->ntiles;
-    const int64_t ld = s->n;
     const unsigned g0 = s->grid[0], g1 = s->grid[1], g2 = s->grid[2];
+    const Geo &g = s->geo;
     if (s->fused) {
-        cg_spmv_pq<M, true><<<g0, SpTraits<M>::THREADS, 0, st>>>(s->A, s->p, s->q, ld, s->part, s->ntiles,
-                                                             s->st, h, use_cond);
-        cg_update<M, true><<<g1, TILE_THREADS, 0, st>>>(s->n, s->x, s->r, s->p, s->q, ld, s->part,
-                                                         s->ntiles, s->st, h, use_cond);
+        cg_spmv_pq<M, true><<<g0, SpTraits<M>::THREADS, 0, st>>>(s->A, s->p, s->q, g, s->part, s->st, h,
+                                                                 use_cond);
+        cg_update<M, true><<<g1, TILE_THREADS, 0, st>>>(s->x, s->r, s->p, s->q, g, s->part, s->st, h,
+                                                         use_cond);
     } else {
         const unsigned pb = (unsigned)((s->parts + 127) / 128);
-        cg_spmv_pq<M, false><<<g0, SpTraits<M>::THREADS, 0, st>>>(s->A, s->p, s->q, ld, s->part, s->ntiles,
-                                                           s->st, h, use_cond);
-        cg_dot_part<M><<<pb, 128, 0, st>>>(s->n, s->p, s->q, ld, s->parts, s->part, s->st, 1);
+        cg_spmv_pq<M, false><<<g0, SpTraits<M>::THREADS, 0, st>>>(s->A, s->p, s->q, g, s->part, s->st, h,
+                                                                  use_cond);
+        cg_dot_part<M><<<pb, 128, 0, st>>>(s->n, s->p, s->q, s->n, s->parts, s->part, s->st, 1);
         cg_ref_combine<M><<<1, 1, 0, st>>>(s->part, s->parts, s->st, 1, h, use_cond);
-        cg_update<M, false><<<g1, TILE_THREADS, 0, st>>>(s->n, s->x, s->r, s->p, s->q, ld, s->part,
-                                                          s->ntiles, s->st, h, use_cond);
-        cg_dot_part<M><<<pb, 128, 0, st>>>(s->n, s->r, s->r, ld, s->parts, s->part, s->st, 1);
+        cg_update<M, false><<<g1, TILE_THREADS, 0, st>>>(s->x, s->r, s->p, s->q, g, s->part, s->st, h,
+                                                          use_cond);
+        cg_dot_part<M><<<pb, 128, 0, st>>>(s->n, s->r, s->r, s->n, s->parts, s->part, s->st, 1);
         cg_ref_combine<M><<<1, 1, 0, st>>>(s->part, s->parts, s->st, 2, h, use_cond);
     }
-    cg_xpay<M><<<g2, TILE_THREADS, 0, st>>>(s->n, s->p, s->r, ld, s->ntiles, s->st, h, use_cond);
-    (void)tiles;
+    cg_xpay<M><<<g2, TILE_THREADS, 0, st>>>(s->p, s->r, g, s->st, h, use_cond);
     MWCG_CHECK_LAUNCH();
     return 0;
 }
@@ -522,15 +558,42 @@ template <int M>
 int enqueue_init(mwcg_solver *s) {
     cudaStream_t st = s->stream;
     const unsigned tiles = s->grid[3];
+    const Geo &g = s->geo;
     if (s->fused) {
-        cg_init<M, true><<<tiles, TILE_THREADS, 0, st>>>(s->n, s->b, s->q, s->r, s->p, s->n, s->part,
-                                                          s->ntiles, s->st);
+        cg_init<M, true><<<tiles, TILE_THREADS, 0, st>>>(s->b, s->q, s->r, s->p, g, s->part, s->st);
     } else {
         const unsigned pb = (unsigned)((s->parts + 127) / 128);
-        cg_init<M, false><<<tiles, TILE_THREADS, 0, st>>>(s->n, s->b, s->q, s->r, s->p, s->n, s->part,
-                                                           s->ntiles, s->st);
+        cg_init<M, false><<<tiles, TILE_THREADS, 0, st>>>(s->b, s->q, s->r, s->p, g, s->part, s->st);
         cg_dot_part<M><<<pb, 128, 0, st>>>(s->n, s->r, s->r, s->n, s->parts, s->part, s->st, 0);
         cg_ref_combine<M><<<1, 1, 0, st>>>(s->part, s->parts, s->st, 0, cudaGraphConditionalHandle{}, 0);
+    }
+    MWCG_CHECK_LAUNCH();
+    return 0;
+}
+
+// one stage of a multi-rank iteration (dist.py drives the exchanges between them)
+template <int M>
+int enqueue_dist_stage(mwcg_solver *s, int stage) {
+    cudaStream_t st = s->stream;
+    const Geo &g = s->geo;
+    cudaGraphConditionalHandle h{};
+    switch (stage) {
+    case MWCG_STAGE_INIT:
+        cg_init<M, true><<<s->grid[3], TILE_THREADS, 0, st>>>(s->b, s->q, s->r, s->p, g, s->part, s->st);
+        break;
+    case MWCG_STAGE_FINAL_INIT: cg_finalize<M><<<1, TILE_THREADS, 0, st>>>(s->part, g, s->st, 0); break;
+    case MWCG_STAGE_SPMV:
+        cg_spmv_pq<M, true><<<s->grid[0], SpTraits<M>::THREADS, 0, st>>>(s->A, s->p, s->q, g, s->part, s->st,
+                                                                         h, 0);
+        break;
+    case MWCG_STAGE_FINAL_ALPHA: cg_finalize<M><<<1, TILE_THREADS, 0, st>>>(s->part, g, s->st, 1); break;
+    case MWCG_STAGE_UPDATE:
+        cg_update<M, true><<<s->grid[1], TILE_THREADS, 0, st>>>(s->x, s->r, s->p, s->q, g, s->part, s->st, h,
+                                                                 0);
+        break;
+    case MWCG_STAGE_FINAL_BETA: cg_finalize<M><<<1, TILE_THREADS, 0, st>>>(s->part, g, s->st, 2); break;
+    case MWCG_STAGE_XPAY: cg_xpay<M><<<s->grid[2], TILE_THREADS, 0, st>>>(s->p, s->r, g, s->st, h, 0); break;
+    default: set_error("unknown stage %d", stage); return MWCG_ERR_VALUE;
     }
     MWCG_CHECK_LAUNCH();
     return 0;
@@ -554,7 +617,7 @@ int compute_grids_t(mwcg_solver *s) {
     MWCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb[2], cg_xpay<M>, TILE_THREADS, 0));
     for (int i = 0; i < 4; i++) {
         int64_t g = (int64_t)(nb[i] > 0 ? nb[i] : 1) * sms;
-        if (g > s->ntiles) g = s->ntiles;
+        if (g > s->geo.ntiles) g = s->geo.ntiles;
         s->grid[i] = (unsigned)(g > 0 ? g : 1);
     }
     return 0;
@@ -599,9 +662,11 @@ void free_solver(mwcg_solver *s) {
     cudaStream_t st = s->stream;
     if (s->own_x) pool_free(s->x, st);
     pool_free(s->r, st);
-    pool_free(s->p, st);
     pool_free(s->q, st);
-    pool_free(s->part, st);
+    if (!s->dist) {  // caller-owned in the distributed solver
+        pool_free(s->p, st);
+        pool_free(s->part, st);
+    }
     pool_free(s->st, st);
     pool_free(s->xt, st);
     pool_free(s->res, st);
@@ -700,6 +765,7 @@ int mwcg_solver_create(mwcg_solver **out, const mwcg_matrix *A, const mwcg_solve
     s->fused = cfg->reduction != MWCG_RED_PARTITIONS;
     s->parts = s->fused ? 1 : cfg->partitions;
     s->stream = (cudaStream_t)stream;
+    s->geo = Geo{s->n, s->n, s->n, 0, s->ntiles, 0, s->ntiles, s->ntiles, 1};
     const size_t vbytes = sizeof(double) * (size_t)s->W * (size_t)(s->n > 0 ? s->n : 1);
     int rc = 0;
 #define TRY(call)                                  \
@@ -747,6 +813,92 @@ int mwcg_solver_create(mwcg_solver **out, const mwcg_matrix *A, const mwcg_solve
     return 0;
 }
 
+// Rank of a row partition.  A: the rank's rows with GLOBAL
+// column indices.  p_full: caller-owned (w, ldp) replica of p; part:
+// caller-owned (w, part_ld) tile partials of all ranks.  The caller gathers
+// them between stages (dist.py).
+int mwcg_solver_create_dist(mwcg_solver **out, const mwcg_matrix *A, const mwcg_solver_config *cfg,
+                            double *x, double *p_full, int64_t ldp, int64_t p_off, double *part,
+                            int64_t part_ld, int64_t tile_off, int64_t ntiles_glob, void *stream) {
+    if (!out || !A || !cfg || !x || !p_full || !part) {
+        set_error("null argument");
+        return MWCG_ERR_VALUE;
+    }
+    if (!valid_mode(cfg->mode) || cfg->reduction != MWCG_RED_TILE) {
+        set_error("distributed solver: bad mode or reduction (tile order only)");
+        return MWCG_ERR_VALUE;
+    }
+    const int64_t n = A->M->view.n_rows;
+    if (p_off < 0 || p_off + n > ldp || tile_off < 0 || tile_off + num_tiles(n) > part_ld ||
+        ntiles_glob > part_ld || A->M->view.n_cols > ldp) {
+        set_error("distributed solver: inconsistent geometry");
+        return MWCG_ERR_VALUE;
+    }
+    auto *s = new mwcg_solver();
+    s->A = A->M->view;
+    s->mode = cfg->mode;
+    s->W = words_of(cfg->mode);
+    s->cfg = *cfg;
+    s->n = n;
+    s->ntiles = num_tiles(n);
+    s->fused = true;
+    s->dist = true;
+    s->stream = (cudaStream_t)stream;
+    s->x = x;
+    s->p = p_full;
+    s->part = part;
+    s->geo = Geo{n, n, ldp, p_off, s->ntiles, tile_off, part_ld, ntiles_glob, 0};
+    const size_t vbytes = sizeof(double) * (size_t)s->W * (size_t)(n > 0 ? n : 1);
+#define TRY(call)                                                \
+    do {                                                         \
+        cudaError_t e_ = (call);                                 \
+        if (e_ != cudaSuccess) {                                 \
+            set_error("%s: %s", #call, cudaGetErrorString(e_));  \
+            s->p = nullptr;                                      \
+            s->part = nullptr;                                   \
+            free_solver(s);                                      \
+            return (int)e_;                                      \
+        }                                                        \
+    } while (0)
+    TRY(pool_alloc((void **)&s->r, vbytes, s->stream));
+    TRY(pool_alloc((void **)&s->q, vbytes, s->stream));
+    TRY(pool_alloc((void **)&s->st, sizeof(CgState), s->stream));
+    TRY(cudaMemsetAsync(s->st, 0, sizeof(CgState), s->stream));
+    TRY(cudaMallocHost((void **)&s->st_host, sizeof(CgState) + 16 * sizeof(double)));
+    s->kstop_host = (long long *)((char *)s->st_host + sizeof(CgState));
+    s->mout_host = (double *)((char *)s->st_host + sizeof(CgState) + 2 * sizeof(double));
+    for (auto &e : s->ev) TRY(cudaEventCreate(&e));
+#undef TRY
+    if (n > 0) {
+        int rc = compute_grids(s);
+        if (rc) {
+            s->p = nullptr;
+            s->part = nullptr;
+            free_solver(s);
+            return rc;
+        }
+    }
+    *out = s;
+    return 0;
+}
+
+int mwcg_solver_dist_stage(mwcg_solver *s, int stage) {
+    if (!s || !s->dist) {
+        set_error("not a distributed solver");
+        return MWCG_ERR_STATE;
+    }
+    if (s->n == 0 && (stage == MWCG_STAGE_INIT || stage == MWCG_STAGE_SPMV || stage == MWCG_STAGE_UPDATE ||
+                      stage == MWCG_STAGE_XPAY))
+        return 0;  // a rank without rows still takes part in the finalize stages
+    switch (s->mode) {
+    case FP64: return enqueue_dist_stage<FP64>(s, stage);
+    case DW: return enqueue_dist_stage<DW>(s, stage);
+    case QDW: return enqueue_dist_stage<QDW>(s, stage);
+    case TW: return enqueue_dist_stage<TW>(s, stage);
+    default: return enqueue_dist_stage<QTW>(s, stage);
+    }
+}
+
 int mwcg_solver_destroy(mwcg_solver *s) {
     free_solver(s);
     return 0;
@@ -775,7 +927,7 @@ int mwcg_solver_start(mwcg_solver *s, const double *b, double b_norm, const doub
     init.status = RUNNING;
     *s->st_host = init;
     MWCG_CUDA(cudaMemcpyAsync(s->st, s->st_host, sizeof(CgState), cudaMemcpyHostToDevice, st));
-    if (s->n == 0) {
+    if (s->n == 0 && !s->dist) {
         // empty system: rho = 0 -> rel = 0 < eps -> converged at 0
         s->st_host->status = CONVERGED;
         s->st_host->rel = 0.0;
@@ -783,8 +935,31 @@ int mwcg_solver_start(mwcg_solver *s, const double *b, double b_norm, const doub
         return 0;
     }
     MWCG_CUDA(cudaMemsetAsync(s->x, 0, vbytes, st));
-    if (x0) MWCG_CUDA(cudaMemcpyAsync(s->x, x0, sizeof(double) * (size_t)s->n, cudaMemcpyDeviceToDevice, st));
-    int rc = launch_spmv(s->mode, s->A, s->x, s->n, s->q, s->n, st);
+    int rc = 0;
+    if (!s->dist) {
+        if (x0) MWCG_CUDA(cudaMemcpyAsync(s->x, x0, sizeof(double) * (size_t)s->n, cudaMemcpyDeviceToDevice, st));
+        rc = launch_spmv(s->mode, s->A, s->x, s->n, s->q, s->n, st);
+    } else {
+        // x0 is the FULL (global, padded) initial guess on every rank: the
+        // local slice seeds x; the SpMV reads the replica through p's buffer
+        // (p is overwritten by the init stage right after).
+        const int64_t ldp = s->geo.ldp;
+        MWCG_CUDA(cudaMemsetAsync(s->p, 0, sizeof(double) * (size_t)s->W * (size_t)ldp, st));
+        if (x0) {
+            MWCG_CUDA(cudaMemcpyAsync(s->x, x0 + s->geo.p_off, sizeof(double) * (size_t)s->n,
+                                      cudaMemcpyDeviceToDevice, st));
+            MWCG_CUDA(cudaMemcpyAsync(s->p, x0, sizeof(double) * (size_t)ldp, cudaMemcpyDeviceToDevice, st));
+        }
+        rc = launch_spmv(s->mode, s->A, s->p, ldp, s->q, s->n, st);
+        if (rc) return rc;
+        switch (s->mode) {  // local init stage only; dist.py gathers + finalizes
+        case FP64: return enqueue_dist_stage<FP64>(s, MWCG_STAGE_INIT);
+        case DW: return enqueue_dist_stage<DW>(s, MWCG_STAGE_INIT);
+        case QDW: return enqueue_dist_stage<QDW>(s, MWCG_STAGE_INIT);
+        case TW: return enqueue_dist_stage<TW>(s, MWCG_STAGE_INIT);
+        default: return enqueue_dist_stage<QTW>(s, MWCG_STAGE_INIT);
+        }
+    }
     if (rc) return rc;
     switch (s->mode) {
     case FP64: rc = enqueue_init<FP64>(s); break;
@@ -833,35 +1008,29 @@ int mwcg_solver_run_profiled(mwcg_solver *s, int64_t k_stop, double *ms) {
 #define STAGES(Mx)                                                                                         \
     do {                                                                                                   \
         const unsigned pb = (unsigned)((s->parts + 127) / 128);                                            \
+        const Geo &g = s->geo;                                                                             \
         if (s->fused) {                                                                                    \
-            cg_spmv_pq<Mx, true><<<s->grid[0], SpTraits<Mx>::THREADS, 0, st>>>(s->A, s->p, s->q, s->n, s->part,     \
-                                                                  s->ntiles, s->st, h, 0);                 \
+            cg_spmv_pq<Mx, true><<<s->grid[0], SpTraits<Mx>::THREADS, 0, st>>>(s->A, s->p, s->q, g,        \
+                                                                              s->part, s->st, h, 0);       \
         } else {                                                                                           \
-            cg_spmv_pq<Mx, false><<<s->grid[0], SpTraits<Mx>::THREADS, 0, st>>>(s->A, s->p, s->q, s->n, s->part,    \
-                                                                   s->ntiles, s->st, h, 0);                \
+            cg_spmv_pq<Mx, false><<<s->grid[0], SpTraits<Mx>::THREADS, 0, st>>>(s->A, s->p, s->q, g,       \
+                                                                               s->part, s->st, h, 0);      \
             cg_dot_part<Mx><<<pb, 128, 0, st>>>(s->n, s->p, s->q, s->n, s->parts, s->part, s->st, 1);      \
             cg_ref_combine<Mx><<<1, 1, 0, st>>>(s->part, s->parts, s->st, 1, h, 0);                        \
         }                                                                                                  \
         cudaEventRecord(s->ev[1], st);                                                                     \
         if (s->fused) {                                                                                    \
-            cg_update<Mx, true><<<s->grid[1], TILE_THREADS, 0, st>>>(s->n, s->x, s->r, s->p, s->q, s->n,   \
-                                                                 s->part, s->ntiles, s->st, h, 0);         \
+            cg_update<Mx, true><<<s->grid[1], TILE_THREADS, 0, st>>>(s->x, s->r, s->p, s->q, g, s->part,   \
+                                                                      s->st, h, 0);                        \
         } else {                                                                                           \
-            cg_update<Mx, false><<<s->grid[1], TILE_THREADS, 0, st>>>(s->n, s->x, s->r, s->p, s->q, s->n,  \
-                                                                  s->part, s->ntiles, s->st, h, 0);        \
+            cg_update<Mx, false><<<s->grid[1], TILE_THREADS, 0, st>>>(s->x, s->r, s->p, s->q, g, s->part,  \
+                                                                       s->st, h, 0);                       \
             cg_dot_part<Mx><<<pb, 128, 0, st>>>(s->n, s->r, s->r, s->n, s->parts, s->part, s->st, 1);      \
             cg_ref_combine<Mx><<<1, 1, 0, st>>>(s->part, s->parts, s->st, 2, h, 0);                        \
         }                                                                                                  \
         cudaEventRecord(s->ev[2], st);                                                                     \
-        cg_xpay<Mx><<<s->grid[2], TILE_THREADS, 0, st>>>(s->n, s->p, s->r, s->n, s->ntiles, s->st, h, 0); \
+        cg_xpay<Mx><<<s->grid[2], TILE_THREADS, 0, st>>>(s->p, s->r, g, s->st, h, 0);                     \
     } while (0)
-        switch (s->mode) {
-        case FP64: STAGES(FP64); break;
-        case DW: STAGES(DW); break;
-        case QDW: STAGES(QDW); break;
-        case TW: STAGES(TW); break;
-        default: STAGES(QTW); break;
-        }
 #undef STAGES
         MWCG_CHECK_LAUNCH();
         MWCG_CUDA(cudaEventRecord(s->ev[3], st));
@@ -909,6 +1078,11 @@ int mwcg_solver_metrics(mwcg_solver *s, double *err, double *true_res) {
     }
     cudaStream_t st = s->stream;
     const int64_t n = s->n;
+    if (s->dist) {  // TW metrics of a partitioned iterate: not implemented (NaN)
+        if (err) *err = NAN;
+        if (true_res) *true_res = NAN;
+        return 0;
+    }
     if (n == 0) {
         if (err) *err = s->x_star ? 0.0 : NAN;
         if (true_res) *true_res = 0.0;
