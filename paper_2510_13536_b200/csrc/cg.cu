@@ -234,11 +234,22 @@ __global__ void __launch_bounds__(SpTraits<M>::THREADS, SpTraits<M>::MINB)
 // registers go to occupancy instead.
 template <int M>
 struct Hoist {
+#ifdef MWCG_UP_HOIST_OVERRIDE
+    static constexpr int value = (M == TW) ? 1 : MWCG_UP_HOIST_OVERRIDE;
+#else
     static constexpr int value = (M == TW) ? 1 : (Arith<M>::W == 3 ? 2 : TILE_ELEMS);
+#endif
+#ifdef MWCG_UP_MINB_OVERRIDE
+    static constexpr int MINB = MWCG_UP_MINB_OVERRIDE;
+#else
+    // an explicit minimum is needed: with (256, 1) ptxas spends up to 255
+    // registers and halves occupancy
+    static constexpr int MINB = (M == TW) ? 3 : 2;
+#endif
 };
 
 template <int M, bool FUSED>
-__global__ void __launch_bounds__(TILE_THREADS)
+__global__ void __launch_bounds__(TILE_THREADS, Hoist<M>::MINB)
     cg_update(double *__restrict__ x, double *__restrict__ r, const double *__restrict__ p,
               const double *__restrict__ q, Geo g, double *__restrict__ part, CgState *st,
               cudaGraphConditionalHandle h, int use_cond) {
@@ -1031,6 +1042,13 @@ int mwcg_solver_run_profiled(mwcg_solver *s, int64_t k_stop, double *ms) {
         cudaEventRecord(s->ev[2], st);                                                                     \
         cg_xpay<Mx><<<s->grid[2], TILE_THREADS, 0, st>>>(s->p, s->r, g, s->st, h, 0);                     \
     } while (0)
+        switch (s->mode) {
+        case FP64: STAGES(FP64); break;
+        case DW: STAGES(DW); break;
+        case QDW: STAGES(QDW); break;
+        case TW: STAGES(TW); break;
+        default: STAGES(QTW); break;
+        }
 #undef STAGES
         MWCG_CHECK_LAUNCH();
         MWCG_CUDA(cudaEventRecord(s->ev[3], st));

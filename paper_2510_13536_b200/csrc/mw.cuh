@@ -131,7 +131,7 @@ MWI V<2> norm_dw(V<2> a) {
 // NaN and both forms give NaN.  Step 0 therefore costs one DADD
 // (CHAIN = true).
 template <int N, int M, bool CHAIN = true>
-MWI V<3> vseb(const double (&e)[N]) {
+MWI V<3> vseb_general(const double (&e)[N]) {
     double r0 = 0.0, r1 = 0.0, r2 = 0.0;
     int cnt = 0;
     bool done = false;
@@ -160,6 +160,11 @@ MWI V<3> vseb(const double (&e)[N]) {
         if (M == 3) r2 = (cnt == 2) ? eps : r2;
     }
     return V<3>{{r0, r1, r2}};
+}
+
+template <int N, int M, bool CHAIN = true>
+MWI V<3> vseb(const double (&e)[N]) {
+    return vseb_general<N, M, CHAIN>(e);
 }
 
 // _vec_sum: multiword.py:175-184 (bottom-up chained TwoSum)

@@ -10,6 +10,7 @@
 #include <vector>
 #include <cstdlib>
 #include <cuda_runtime.h>
+#include "mw.cuh"
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s: %s\n", #x, cudaGetErrorString(e)); return 1; } } while (0)
 
@@ -54,6 +55,38 @@ __global__ void sell_kernel(const int64_t *__restrict__ sp, const int *__restric
             for (int u = 0; u < 8; u++) if (u < len[q]) s = __dadd_rn(s, __dmul_rn(a[q][u], xv[u]));
             int64_t row = base + q * stride;
             if (row < n) y[row] = s;
+        }
+    }
+}
+
+// DW variant: two word planes, dxdw_mul + dw_add chain, optional sentinel (no row_len)
+template <int RPT, bool SENT>
+__global__ void __launch_bounds__(256) sell_dw_kernel(const int64_t *__restrict__ sp, const int *__restrict__ rl,
+                                      const int *__restrict__ cols, const double *__restrict__ vals,
+                                      const double *__restrict__ x, double *__restrict__ y, int64_t n) {
+    int64_t r0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
+    int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = r0; base < n; base += stride * RPT) {
+#pragma unroll
+        for (int q = 0; q < RPT; q++) {
+            int64_t row = base + q * stride;
+            if (row >= n) break;
+            int len = SENT ? 8 : __ldcs(rl + row);
+            int64_t off = __ldg(sp + (row >> 5)) + (row & 31);
+            int c[8]; double a[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                int kk = SENT ? u : min(u, max(len - 1, 0));
+                c[u] = __ldcs(cols + off + kk * 32);
+                a[u] = __ldcs(vals + off + kk * 32);
+            }
+            mw::V<2> s = mw::zero<2>();
+            mw::V<2> xv[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) { int cc = SENT ? max(c[u], 0) : c[u]; xv[u] = mw::V<2>{{__ldg(x + cc), __ldg(x + n + cc)}}; }
+#pragma unroll
+            for (int u = 0; u < 8; u++) if (SENT ? (c[u] >= 0) : (u < len)) s = mw::dw_add(s, mw::dxdw_mul(a[u], xv[u]));
+            y[row] = s.w[0]; y[n + row] = s.w[1];
         }
     }
 }
@@ -124,6 +157,18 @@ int main() {
         timeit(nm, sbytes, [&] { sell_kernel<true, 1><<<sms * bps, 256>>>(d_sp, d_rl, d_c, d_v, d_x, d_y, n); });
         snprintf(nm, 64, "D sell gather rpt2 (blocks/SM=%d)", bps);
         timeit(nm, sbytes, [&] { sell_kernel<true, 2><<<sms * bps, 256>>>(d_sp, d_rl, d_c, d_v, d_x, d_y, n); });
+    }
+    {
+        double *d_x2, *d_y2; CK(cudaMalloc(&d_x2, 16 * n)); CK(cudaMalloc(&d_y2, 16 * n)); CK(cudaMemset(d_x2, 0, 16 * n));
+        double dbytes = mbytes + 4.0 * n + 16.0 * n * 2;
+        for (int bps : {2, 4, 6, 8}) {
+            char nm[64];
+            snprintf(nm, 64, "DW sell gather rpt1 (blocks/SM=%d)", bps);
+            timeit(nm, dbytes, [&] { sell_dw_kernel<1, false><<<sms * bps, 256>>>(d_sp, d_rl, d_c, d_v, d_x2, d_y2, n); });
+            snprintf(nm, 64, "DW sell gather rpt2 (blocks/SM=%d)", bps);
+            timeit(nm, dbytes, [&] { sell_dw_kernel<2, false><<<sms * bps, 256>>>(d_sp, d_rl, d_c, d_v, d_x2, d_y2, n); });
+        }
+        timeit("DW sell grid=n/256", dbytes, [&] { sell_dw_kernel<1, false><<<(unsigned)((n + 255) / 256), 256>>>(d_sp, d_rl, d_c, d_v, d_x2, d_y2, n); });
     }
     // one-row-per-thread, full grid (no persistence)
     timeit("C' sell gather, grid = n/256", sbytes, [&] { sell_kernel<true, 1><<<(unsigned)((n + 255) / 256), 256>>>(d_sp, d_rl, d_c, d_v, d_x, d_y, n); });
