@@ -1,0 +1,56 @@
+"""Summarise ncu reports / launch lists into profiles/ (tracked)."""
+import csv
+import json
+import subprocess
+import sys
+
+KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+        "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed.avg.per_cycle_active", "launch__registers_per_thread",
+        "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+        "l1tex__t_sector_hit_rate.pct", "lts__t_sector_hit_rate.pct", "smsp__inst_executed.sum"]
+
+
+def report(path):
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(out.splitlines()))
+    hdr, units = rows[0], rows[1]
+    res = []
+    for r in rows[2:]:
+        d = dict(zip(hdr, r))
+        u = dict(zip(hdr, units))
+        e = {"kernel": d["Kernel Name"][:80]}
+        for k in KEYS:
+            if k in d:
+                e[k] = f"{d[k]} {u[k]}".strip()
+        stalls = sorted(((k.replace("smsp__average_warps_issue_stalled_", "").replace(
+            "_per_issue_active.ratio", ""), float(d[k])) for k in hdr
+            if k.startswith("smsp__average_warps_issue_stalled") and k.endswith("per_issue_active.ratio")
+            and d[k].replace(".", "", 1).isdigit()), key=lambda kv: -kv[1])[:6]
+        e["top_stalls"] = stalls
+        res.append(e)
+    return res
+
+
+def launches(path):
+    rows = list(csv.reader(open(path)))
+    hdr, data = None, {}
+    for r in rows:
+        if r and r[0] == "ID":
+            hdr = r
+            continue
+        if hdr and len(r) == len(hdr):
+            d = dict(zip(hdr, r))
+            key = (int(d["ID"]), d["Kernel Name"][:60])
+            data.setdefault(key, {})[d["Metric Name"]] = f"{d['Metric Value']} {d['Metric Unit']}"
+    return [{"id": k[0], "kernel": k[1], **v} for k, v in sorted(data.items())]
+
+
+if __name__ == "__main__":
+    kind, src, dst = sys.argv[1:4]
+    obj = report(src) if kind == "report" else launches(src)
+    with open(dst, "w") as f:
+        json.dump(obj, f, indent=1)
+    print("wrote", dst, len(obj))
