@@ -52,6 +52,9 @@ SIGNATURES = {
     "mwcg_device_check": (ctypes.c_int, []),
     "mwcg_matrix_create": (ctypes.c_int, [ctypes.POINTER(c_vp), c_i64, c_i64, c_i64, c_vp, c_vp,
                                           c_vp, ctypes.c_int, c_vp]),
+    "mwcg_matrix_create_ex": (ctypes.c_int, [ctypes.POINTER(c_vp), c_i64, c_i64, c_i64, c_vp, c_vp,
+                                             c_vp, ctypes.c_int, c_i64, ctypes.c_int, c_vp]),
+    "mwcg_matrix_col_bytes": (ctypes.c_int, [c_vp]),
     "mwcg_matrix_destroy": (ctypes.c_int, [c_vp]),
     "mwcg_matrix_info": (ctypes.c_int, [c_vp, ctypes.POINTER(c_i64), ctypes.POINTER(c_i64),
                                         ctypes.POINTER(c_i64), ctypes.POINTER(c_i64)]),

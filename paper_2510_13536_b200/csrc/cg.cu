@@ -710,13 +710,26 @@ int mwcg_matrix_create(mwcg_matrix **out, int64_t n_rows, int64_t n_cols, int64_
         set_error("null output handle");
         return MWCG_ERR_VALUE;
     }
+    return mwcg_matrix_create_ex(out, n_rows, n_cols, nnz, row_ptr, col_idx, values, index_bytes, 0, -1,
+                                 stream);
+}
+
+int mwcg_matrix_create_ex(mwcg_matrix **out, int64_t n_rows, int64_t n_cols, int64_t nnz, const void *row_ptr,
+                          const void *col_idx, const double *values, int index_bytes, int64_t row_base,
+                          int col_format, void *stream) {
+    if (!out) {
+        set_error("null output handle");
+        return MWCG_ERR_VALUE;
+    }
     SellMatrixOwned *M = nullptr;
-    int rc = sell_create(&M, n_rows, n_cols, nnz, row_ptr, col_idx, values, index_bytes,
+    int rc = sell_create(&M, n_rows, n_cols, nnz, row_ptr, col_idx, values, index_bytes, row_base, col_format,
                          (cudaStream_t)stream);
     if (rc) return rc;
     *out = new mwcg_matrix{M};
     return 0;
 }
+
+int mwcg_matrix_col_bytes(const mwcg_matrix *A) { return A ? (A->M->view.col16 ? 2 : 4) : -1; }
 
 int mwcg_matrix_destroy(mwcg_matrix *A) {
     if (A) {

@@ -24,18 +24,27 @@ inline int64_t num_tiles(int64_t n) { return (n + TILE - 1) / TILE; }
 
 // SELL-32 matrix (built on device from CSR, sell.cu).  Entry k of row r sits
 // at slice_ptr[r/32] + k*32 + r%32 (column-major inside a slice), so a warp
-// walking its 32 rows in lock-step issues coalesced 128-B/256-B loads while
-// each thread keeps the reference's strict left-to-right order inside its row
-// (kernels.py:175-180).  Padding slots are never read (loop bound row_len).
+// walking its 32 rows in lock-step issues coalesced loads while each thread
+// keeps the reference's strict left-to-right order inside its row
+// (kernels.py:175-180).  Padding slots (after a row's last entry) hold a
+// SENTINEL column, so no per-row length array is stored or loaded.
+//
+// Column storage: when every |col - (row_base + row)| < 2^15 (stencils,
+// banded matrices) the columns are int16 deltas (2 B/entry instead of 4;
+// sentinel INT16_MIN), otherwise absolute int32 (sentinel -1).
+constexpr int16_t COL16_SENT = -32768;
+constexpr int32_t COL32_SENT = -1;
+
 struct SellMatrix {
     int64_t n_rows;
     int64_t n_cols;
     int64_t nnz;
     int64_t n_slices;
     int64_t total;          // padded entry count
+    int64_t row_base;       // global index of local row 0 (row-partitioned ranks)
+    int col16;              // 1: int16 deltas, 0: int32 absolute
     const int64_t *slice_ptr;
-    const int32_t *row_len;
-    const int32_t *cols;
+    const void *cols;
     const double *vals;
 };
 

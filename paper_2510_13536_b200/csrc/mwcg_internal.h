@@ -13,15 +13,15 @@ namespace mwcg {
 
 struct SellMatrixOwned {
     SellMatrix view{};
-    int32_t *row_len = nullptr;
     int64_t *slice_ptr = nullptr;
-    int32_t *cols = nullptr;
+    void *cols = nullptr;
     double *vals = nullptr;
 };
 
+// col_format: -1 auto (int16 deltas when they fit), 0 force int32, 1 force int16
 int sell_create(SellMatrixOwned **out, int64_t n_rows, int64_t n_cols, int64_t nnz,
                 const void *row_ptr, const void *col_idx, const double *values, int index_bytes,
-                cudaStream_t st);
+                int64_t row_base, int col_format, cudaStream_t st);
 void sell_destroy(SellMatrixOwned *M);
 
 // operator-level launches (ops.cu); all stream-ordered

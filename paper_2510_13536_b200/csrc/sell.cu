@@ -2,34 +2,52 @@
 // -> device SELL-32 layout (common.cuh: SellMatrix).
 //
 // The reference keeps CSR and walks rows with one scalar thread.  On B200 the
-// SpMV is HBM-bound, so the layout is chosen for coalescing: slices of 32 rows
-// (one warp), entries column-major inside a slice.  Row order of entries is
-// preserved, so the per-row left-to-right accumulation (and hence every bit of
-// the result) is unchanged.
+// SpMV is HBM-bound, so the layout is chosen for coalescing and bytes: slices
+// of 32 rows (one warp), entries column-major inside a slice, padding marked
+// by a sentinel column (no row-length array), and int16 column deltas when
+// the matrix is banded enough.  Row order of entries is preserved, so the
+// per-row left-to-right accumulation (and hence every bit of the result) is
+// unchanged.
 #include <cub/cub.cuh>
 #include "common.cuh"
 #include "mwcg_internal.h"
 
 namespace mwcg {
 
+// slice sizes (32 * max row length in the slice) and the int16 feasibility
+// flag (any |col - row| >= 2^15 -> int32 columns)
 template <typename I>
-__global__ void sell_row_len_kernel(const I *__restrict__ rp, int64_t n_rows, int64_t n_pad,
-                                    int32_t *__restrict__ row_len, int64_t *__restrict__ slice_sz) {
+__global__ void sell_scan_kernel(const I *__restrict__ rp, const I *__restrict__ ci, int64_t n_rows,
+                                 int64_t n_pad, int64_t row_base, int64_t *__restrict__ slice_sz,
+                                 unsigned int *__restrict__ too_wide) {
     int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int len = 0;
-    if (r < n_rows) len = (int)(rp[r + 1] - rp[r]);
-    if (r < n_pad) row_len[r] = len;
-    // slice max via warp reduction (blockDim multiple of 32, slices warp-aligned)
+    bool wide = false;
+    if (r < n_rows) {
+        const int64_t lo = rp[r], hi = rp[r + 1];
+        len = (int)(hi - lo);
+        const int64_t g = row_base + r;
+        for (int64_t k = lo; k < hi; k++) {
+            const int64_t d = (int64_t)ci[k] - g;
+            wide |= (d < -32767 || d > 32767);
+        }
+    }
     int m = len;
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, off));
     if ((threadIdx.x & 31) == 0 && r < n_pad) slice_sz[r >> 5] = (int64_t)m * SLICE;
+    if (__any_sync(0xffffffffu, wide) && (threadIdx.x & 31) == 0) atomicOr(too_wide, 1u);
 }
 
-template <typename I>
+__global__ void fill16_kernel(int16_t *__restrict__ p, int64_t n, int16_t v) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = v;
+}
+
+template <typename I, typename C>
 __global__ void sell_fill_kernel(const I *__restrict__ rp, const I *__restrict__ ci,
-                                 const double *__restrict__ va, int64_t n_rows,
-                                 const int64_t *__restrict__ slice_ptr, int32_t *__restrict__ cols,
+                                 const double *__restrict__ va, int64_t n_rows, int64_t row_base,
+                                 const int64_t *__restrict__ slice_ptr, C *__restrict__ cols,
                                  double *__restrict__ vals) {
     // one warp per row: coalesced reads of the CSR row, strided SELL writes
     int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -40,26 +58,29 @@ __global__ void sell_fill_kernel(const I *__restrict__ rp, const I *__restrict__
     int64_t lo = rp[r], hi = rp[r + 1];
     for (int64_t k = lo + lane; k < hi; k += 32) {
         int64_t kk = k - lo;
-        cols[base + kk * SLICE] = (int32_t)ci[k];
+        if (sizeof(C) == 2) cols[base + kk * SLICE] = (C)((int64_t)ci[k] - (row_base + r));
+        else cols[base + kk * SLICE] = (C)ci[k];
         vals[base + kk * SLICE] = va[k];
     }
 }
 
 template <typename I>
-static int build_sell(SellMatrixOwned *M, const I *rp, const I *ci, const double *va,
+static int build_sell(SellMatrixOwned *M, const I *rp, const I *ci, const double *va, int col_format,
                       cudaStream_t st) {
     SellMatrix &A = M->view;
     int64_t n_pad = A.n_slices * SLICE;
     int64_t *slice_sz = nullptr;
-    MWCG_CUDA(pool_alloc((void **)&M->row_len, sizeof(int32_t) * (n_pad > 0 ? n_pad : 1), st));
+    unsigned int *flag = nullptr;
     MWCG_CUDA(pool_alloc((void **)&M->slice_ptr, sizeof(int64_t) * (A.n_slices + 1), st));
     MWCG_CUDA(pool_alloc((void **)&slice_sz, sizeof(int64_t) * (A.n_slices + 1), st));
+    MWCG_CUDA(pool_alloc((void **)&flag, sizeof(unsigned int), st));
     MWCG_CUDA(cudaMemsetAsync(slice_sz, 0, sizeof(int64_t) * (A.n_slices + 1), st));
+    MWCG_CUDA(cudaMemsetAsync(flag, 0, sizeof(unsigned int), st));
     if (n_pad > 0) {
         int threads = 256;
         int64_t blocks = (n_pad + threads - 1) / threads;
-        sell_row_len_kernel<I><<<(unsigned)blocks, threads, 0, st>>>(rp, A.n_rows, n_pad, M->row_len,
-                                                                     slice_sz);
+        sell_scan_kernel<I><<<(unsigned)blocks, threads, 0, st>>>(rp, ci, A.n_rows, n_pad, A.row_base, slice_sz,
+                                                                  flag);
         MWCG_CHECK_LAUNCH();
     }
     size_t tmp_bytes = 0;
@@ -68,26 +89,42 @@ static int build_sell(SellMatrixOwned *M, const I *rp, const I *ci, const double
     MWCG_CUDA(pool_alloc(&tmp, tmp_bytes, st));
     MWCG_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, slice_sz, M->slice_ptr, A.n_slices + 1, st));
     int64_t total = 0;
-    MWCG_CUDA(cudaMemcpyAsync(&total, M->slice_ptr + A.n_slices, sizeof(int64_t),
-                              cudaMemcpyDeviceToHost, st));
+    unsigned int wide = 0;
+    MWCG_CUDA(cudaMemcpyAsync(&total, M->slice_ptr + A.n_slices, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    MWCG_CUDA(cudaMemcpyAsync(&wide, flag, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
     MWCG_CUDA(cudaStreamSynchronize(st));
     pool_free(tmp, st);
     pool_free(slice_sz, st);
+    pool_free(flag, st);
     A.total = total;
-    MWCG_CUDA(pool_alloc((void **)&M->cols, sizeof(int32_t) * (total > 0 ? total : 1), st));
-    MWCG_CUDA(pool_alloc((void **)&M->vals, sizeof(double) * (total > 0 ? total : 1), st));
-    // padding slots: column 0 / value 0, so chunked readers may load them safely
-    MWCG_CUDA(cudaMemsetAsync(M->cols, 0, sizeof(int32_t) * (total > 0 ? total : 1), st));
-    MWCG_CUDA(cudaMemsetAsync(M->vals, 0, sizeof(double) * (total > 0 ? total : 1), st));
+    if (col_format == 1 && wide) {
+        set_error("column offsets do not fit int16 deltas");
+        return MWCG_ERR_VALUE;
+    }
+    A.col16 = (col_format == 1 || (col_format < 0 && !wide)) ? 1 : 0;
+    const size_t ne = (size_t)(total > 0 ? total : 1);
+    MWCG_CUDA(pool_alloc((void **)&M->cols, ne * (A.col16 ? 2 : 4), st));
+    MWCG_CUDA(pool_alloc((void **)&M->vals, sizeof(double) * ne, st));
+    // padding: sentinel column, value 0
+    if (A.col16) {
+        fill16_kernel<<<148 * 8, 256, 0, st>>>((int16_t *)M->cols, (int64_t)ne, COL16_SENT);
+        MWCG_CHECK_LAUNCH();
+    } else {
+        MWCG_CUDA(cudaMemsetAsync(M->cols, 0xFF, ne * 4, st));  // -1
+    }
+    MWCG_CUDA(cudaMemsetAsync(M->vals, 0, sizeof(double) * ne, st));
     if (A.n_rows > 0) {
         int threads = 256;
         int64_t blocks = (A.n_rows * 32 + threads - 1) / threads;
-        sell_fill_kernel<I><<<(unsigned)blocks, threads, 0, st>>>(rp, ci, va, A.n_rows, M->slice_ptr,
-                                                                  M->cols, M->vals);
+        if (A.col16)
+            sell_fill_kernel<I, int16_t><<<(unsigned)blocks, threads, 0, st>>>(
+                rp, ci, va, A.n_rows, A.row_base, M->slice_ptr, (int16_t *)M->cols, M->vals);
+        else
+            sell_fill_kernel<I, int32_t><<<(unsigned)blocks, threads, 0, st>>>(
+                rp, ci, va, A.n_rows, A.row_base, M->slice_ptr, (int32_t *)M->cols, M->vals);
         MWCG_CHECK_LAUNCH();
     }
     A.slice_ptr = M->slice_ptr;
-    A.row_len = M->row_len;
     A.cols = M->cols;
     A.vals = M->vals;
     MWCG_CUDA(cudaStreamSynchronize(st));
@@ -96,8 +133,8 @@ static int build_sell(SellMatrixOwned *M, const I *rp, const I *ci, const double
 
 int sell_create(SellMatrixOwned **out, int64_t n_rows, int64_t n_cols, int64_t nnz,
                 const void *row_ptr, const void *col_idx, const double *values, int index_bytes,
-                cudaStream_t st) {
-    if (n_rows < 0 || n_cols < 0 || nnz < 0) {
+                int64_t row_base, int col_format, cudaStream_t st) {
+    if (n_rows < 0 || n_cols < 0 || nnz < 0 || row_base < 0) {
         set_error("negative dimensions");
         return MWCG_ERR_VALUE;
     }
@@ -114,9 +151,12 @@ int sell_create(SellMatrixOwned **out, int64_t n_rows, int64_t n_cols, int64_t n
     M->view.n_cols = n_cols;
     M->view.nnz = nnz;
     M->view.n_slices = (n_rows + SLICE - 1) / SLICE;
+    M->view.row_base = row_base;
     int rc = (index_bytes == 8)
-                 ? build_sell<int64_t>(M, (const int64_t *)row_ptr, (const int64_t *)col_idx, values, st)
-                 : build_sell<int32_t>(M, (const int32_t *)row_ptr, (const int32_t *)col_idx, values, st);
+                 ? build_sell<int64_t>(M, (const int64_t *)row_ptr, (const int64_t *)col_idx, values,
+                                       col_format, st)
+                 : build_sell<int32_t>(M, (const int32_t *)row_ptr, (const int32_t *)col_idx, values,
+                                       col_format, st);
     if (rc != 0) {
         sell_destroy(M);
         return rc;
@@ -127,7 +167,6 @@ int sell_create(SellMatrixOwned **out, int64_t n_rows, int64_t n_cols, int64_t n
 
 void sell_destroy(SellMatrixOwned *M) {
     if (!M) return;
-    pool_free(M->row_len, 0);
     pool_free(M->slice_ptr, 0);
     pool_free(M->cols, 0);
     pool_free(M->vals, 0);

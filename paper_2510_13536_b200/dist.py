@@ -94,7 +94,7 @@ class RankSolver:
         self.x = torch.zeros((w, max(self.n, 1)), dtype=torch.float64, device=dev)
         self.p_full = torch.zeros((w, part.ld_full), dtype=torch.float64, device=dev)
         self.partials = torch.zeros((w, part.part_ld), dtype=torch.float64, device=dev)
-        self.dm = device_matrix(A_local)
+        self.dm = device_matrix(A_local, row_base=self.lo)
         L = _lib.load()
         self._L = L
         cfg = _lib.SolverConfigC(_lib.MODE_ID[mode], _lib.NORM_ID[normalization], 0, 0, 1)

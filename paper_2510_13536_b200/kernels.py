@@ -105,8 +105,10 @@ class MultiwordVector:
 
 
 # ---------------------------------------------------------------- matrices
-def device_matrix(A):
-    """SELL-32 device copy of a CsrMatrix, built once and cached on A."""
+def device_matrix(A, row_base=0, col_format=-1):
+    """SELL-32 device copy of a CsrMatrix, built once and cached on A.
+    row_base: global index of row 0 when A holds a rank's rows with global
+    columns (dist.py); col_format: -1 auto / 0 int32 / 1 int16 deltas."""
     h = getattr(A, "_device", None)
     if h is not None:
         return h
@@ -116,9 +118,9 @@ def device_matrix(A):
     ci = torch.from_numpy(np.ascontiguousarray(A.col_idx, dtype=np.int64)).to(dev)
     va = torch.from_numpy(np.ascontiguousarray(A.values, dtype=np.float64)).to(dev)
     handle = ctypes.c_void_p()
-    _lib.check(L.mwcg_matrix_create(ctypes.byref(handle), A.n_rows, A.n_cols, A.nnz,
-                                    _lib.ptr(rp), _lib.ptr(ci), _lib.ptr(va), 8,
-                                    _lib.stream_handle()))
+    _lib.check(L.mwcg_matrix_create_ex(ctypes.byref(handle), A.n_rows, A.n_cols, A.nnz,
+                                       _lib.ptr(rp), _lib.ptr(ci), _lib.ptr(va), 8, int(row_base),
+                                       int(col_format), _lib.stream_handle()))
     dm = _DeviceMatrix(handle, A.n_rows, A.n_cols, A.nnz)
     try:
         object.__setattr__(A, "_device", dm)
@@ -132,6 +134,9 @@ class _DeviceMatrix:
         self.handle = handle
         self.n_rows, self.n_cols, self.nnz = n_rows, n_cols, nnz
         self._fin = weakref.finalize(self, _lib.load().mwcg_matrix_destroy, handle)
+
+    def col_bytes(self):
+        return int(_lib.load().mwcg_matrix_col_bytes(self.handle))
 
     def padded_entries(self):
         out = ctypes.c_int64()

@@ -368,3 +368,25 @@ def test_c2_full_size_iterations_bitwise(mode):
     assert res.iterations == o.iterations == 4
     assert same_bits(res.x.planes.cpu().numpy(), o.x)
     assert same_bits(res.final_recurrence_residual, o.final_recurrence_residual)
+
+
+@pytest.mark.parametrize("mode", orc.MODES)
+def test_int16_delta_and_int32_columns_agree(mode):
+    """The two SELL column encodings (int16 deltas / int32 absolute, both
+    with sentinel padding) give the same bits; a matrix with far columns
+    falls back to int32 automatically."""
+    c = problems.config1()
+    A = c["A"]
+    A16 = CsrMatrix(A.n_rows, A.n_cols, A.row_ptr, A.col_idx, A.values)
+    A32 = CsrMatrix(A.n_rows, A.n_cols, A.row_ptr, A.col_idx, A.values)
+    assert K.device_matrix(A16).col_bytes() == 2
+    assert K.device_matrix(A32, col_format=0).col_bytes() == 4
+    rng = np.random.default_rng(11)
+    x = rng.standard_normal((orc.WORDS[mode], A.n_rows))
+    y16 = K.spmv(A16, _vec(mode, x)).planes.cpu().numpy()
+    y32 = K.spmv(A32, _vec(mode, x)).planes.cpu().numpy()
+    assert same_bits(y16, y32) and same_bits(y16, orc.spmv(mode, A, x))
+    far = random_symmetric(40000, extra_per_row=2, seed=3)
+    assert K.device_matrix(far).col_bytes() == 4
+    xf = rng.standard_normal((orc.WORDS[mode], far.n_rows))
+    assert same_bits(K.spmv(far, _vec(mode, xf)).planes.cpu().numpy(), orc.spmv(mode, far, xf))
