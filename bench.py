@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4"])
     ap.add_argument("--mode", default="dw", choices=MODES)
     ap.add_argument("--no-per-arith", action="store_true")
+    ap.add_argument("--extra-configs", default="",
+                    help="comma list of other BASELINE configs (C1,C3,C4) to solve once per "
+                         "arithmetic and report under 'configs' (not part of value)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--partitioned", action="store_true",
@@ -335,6 +338,40 @@ def run_ours(a):
                 del sv
             torch.cuda.empty_cache()
 
+    # ---- other BASELINE configs (reported, not part of value) ---------------
+    extra = {}
+    for name in [c for c in a.extra_configs.split(",") if c]:
+        ec = load_problem(name)
+        EA, Eb = ec["A"], ec["b"]
+        en, ennz = EA.n_rows, EA.nnz
+        ebd = torch.from_numpy(Eb).cuda()
+        ebn = _b_norm(Eb)
+        rows = {}
+        for m in MODES:
+            sv = Solver(EA, m)
+            r0, _ = sv.solve(ebd, ebn, None, None, ec["epsilon"], ec["max_iterations"], stride)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            r, _ = sv.solve(ebd, ebn, None, None, ec["epsilon"], ec["max_iterations"], stride)
+            e1.record()
+            torch.cuda.synchronize()
+            t = e0.elapsed_time(e1) * 1e-3
+            it = max(1, int(r.iterations))
+            wm = WORDS[m]
+            bw = algorithmic_bytes(en, ennz, wm) * it / t / 1e9
+            fn, fx = FLOPS[m]
+            fl = (fn * ennz + fx * en) * it / t
+            rows[m] = {"iterations": int(r.iterations), "reason": _lib.STATUS[r.status],
+                       "final_rel": r.final_rel, "time_to_solution_s": t,
+                       "us_per_iter": 1e6 * t / it, "hbm_frac": bw / hbm,
+                       "fp64_frac": fl / fp64_peak, "roofline_frac": max(bw / hbm, fl / fp64_peak)}
+            del sv
+            torch.cuda.empty_cache()
+        extra[name] = {"workload": workload_name(ec, "all"), "n": en, "nnz": ennz,
+                       "col_bytes": kernels.device_matrix(EA).col_bytes(), "per_arithmetic": rows}
+        del ec, EA, Eb, ebd
+
     # ---- e2e through the public API with host inputs -------------------------
     e2e = None
     if not a.no_e2e:
@@ -408,6 +445,7 @@ def run_ours(a):
             "clocks": clk.summary(),
             "fp64_peak_tops_measured": fp64_peak / 1e12,
             "per_arithmetic": per,
+            "configs": extra,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -441,7 +479,7 @@ def run_partitioned(a, world, rank, local, dist, torch):
 
     def solve():
         rs.start(b_loc, bn, None, eps, max_it)
-        return dist_cg_solve([rs], ex, bn, eps, max_it, check_every=32)
+        return dist_cg_solve([rs], ex, bn, eps, max_it, check_every=32, graph=True)
 
     for _ in range(max(1, a.warmup)):
         solve()

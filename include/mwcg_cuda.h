@@ -172,7 +172,8 @@ enum {
 int mwcg_solver_create_dist(mwcg_solver **out, const mwcg_matrix *A, const mwcg_solver_config *cfg,
                             double *x, double *p_full, int64_t ldp, int64_t p_off, double *part,
                             int64_t part_ld, int64_t tile_off, int64_t ntiles_glob, void *stream);
-int mwcg_solver_dist_stage(mwcg_solver *s, int stage);
+/* stream: NULL = the solver's stream (graph capture passes the capture stream) */
+int mwcg_solver_dist_stage(mwcg_solver *s, int stage, void *stream);
 
 /* ---- measurement helpers (bench.py) ---- */
 /* FP64 pipe microbenchmark: DFMA chains on all SMs; returns FP64 ops/s

@@ -84,7 +84,7 @@ SIGNATURES = {
     "mwcg_solver_create_dist": (ctypes.c_int, [ctypes.POINTER(c_vp), c_vp,
                                                ctypes.POINTER(SolverConfigC), c_vp, c_vp, c_i64,
                                                c_i64, c_vp, c_i64, c_i64, c_i64, c_vp]),
-    "mwcg_solver_dist_stage": (ctypes.c_int, [c_vp, ctypes.c_int]),
+    "mwcg_solver_dist_stage": (ctypes.c_int, [c_vp, ctypes.c_int, c_vp]),
 }
 
 _lib = None

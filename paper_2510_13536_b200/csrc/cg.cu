@@ -165,7 +165,7 @@ struct SpTraits {
 #endif
 };
 
-template <int M, bool FUSED>
+template <int M, bool FUSED, typename CT>
 __global__ void __launch_bounds__(SpTraits<M>::THREADS, SpTraits<M>::MINB)
     cg_spmv_pq(SellMatrix A, const double *__restrict__ p, double *__restrict__ q, Geo g,
                double *__restrict__ part, CgState *st, cudaGraphConditionalHandle h, int use_cond) {
@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(SpTraits<M>::THREADS, SpTraits<M>::MINB)
             V<W> term = zero<W>();
             if (row < n) {
                 // columns are global: p is the full (replicated) vector
-                V<W> sv = spmv_row<M, SpTraits<M>::U>(A, p, g.ldp, row);
+                V<W> sv = spmv_row<M, SpTraits<M>::U, CT>(A, p, g.ldp, row);
                 if (norm_all) sv = Ar::norm(sv);
                 store<W>(q, g.ld, row, sv);
                 if (FUSED) term = Ar::mul(load_ro<W>(p, g.ldp, g.p_off + row), sv);
@@ -475,13 +475,14 @@ __global__ void promote_fp64_kernel(int64_t n, const double *__restrict__ v, dou
     }
 }
 
+template <typename CT>
 __global__ void __launch_bounds__(TILE_THREADS)
     metrics_vec_kernel(SellMatrix A, const double *__restrict__ xt, const double *__restrict__ b,
                        const double *__restrict__ xs, double *__restrict__ res, double *__restrict__ diff) {
     const int64_t n = A.n_rows;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
-        V<3> qi = spmv_row<TW>(A, xt, n, i);
+        V<3> qi = spmv_row<TW, 8, CT>(A, xt, n, i);
         store<3>(res, n, i, dxtw_add(b[i], neg<3>(qi)));
         if (xs) store<3>(diff, n, i, dxtw_add(xs[i], neg<3>(load<3>(xt, n, i))));
     }
@@ -535,14 +536,22 @@ int enqueue_iteration(mwcg_solver *s, cudaStream_t st, cudaGraphConditionalHandl
     const unsigned g0 = s->grid[0], g1 = s->grid[1], g2 = s->grid[2];
     const Geo &g = s->geo;
     if (s->fused) {
-        cg_spmv_pq<M, true><<<g0, SpTraits<M>::THREADS, 0, st>>>(s->A, s->p, s->q, g, s->part, s->st, h,
-                                                                 use_cond);
+        if (s->A.col16)
+            cg_spmv_pq<M, true, int16_t><<<g0, SpTraits<M>::THREADS, 0, st>>>(s->A, s->p, s->q, g, s->part,
+                                                                              s->st, h, use_cond);
+        else
+            cg_spmv_pq<M, true, int32_t><<<g0, SpTraits<M>::THREADS, 0, st>>>(s->A, s->p, s->q, g, s->part,
+                                                                              s->st, h, use_cond);
         cg_update<M, true><<<g1, TILE_THREADS, 0, st>>>(s->x, s->r, s->p, s->q, g, s->part, s->st, h,
                                                          use_cond);
     } else {
         const unsigned pb = (unsigned)((s->parts + 127) / 128);
-        cg_spmv_pq<M, false><<<g0, SpTraits<M>::THREADS, 0, st>>>(s->A, s->p, s->q, g, s->part, s->st, h,
-                                                                  use_cond);
+        if (s->A.col16)
+            cg_spmv_pq<M, false, int16_t><<<g0, SpTraits<M>::THREADS, 0, st>>>(s->A, s->p, s->q, g, s->part,
+                                                                               s->st, h, use_cond);
+        else
+            cg_spmv_pq<M, false, int32_t><<<g0, SpTraits<M>::THREADS, 0, st>>>(s->A, s->p, s->q, g, s->part,
+                                                                               s->st, h, use_cond);
         cg_dot_part<M><<<pb, 128, 0, st>>>(s->n, s->p, s->q, s->n, s->parts, s->part, s->st, 1);
         cg_ref_combine<M><<<1, 1, 0, st>>>(s->part, s->parts, s->st, 1, h, use_cond);
         cg_update<M, false><<<g1, TILE_THREADS, 0, st>>>(s->x, s->r, s->p, s->q, g, s->part, s->st, h,
@@ -594,8 +603,12 @@ int enqueue_dist_stage(mwcg_solver *s, int stage) {
         break;
     case MWCG_STAGE_FINAL_INIT: cg_finalize<M><<<1, TILE_THREADS, 0, st>>>(s->part, g, s->st, 0); break;
     case MWCG_STAGE_SPMV:
-        cg_spmv_pq<M, true><<<s->grid[0], SpTraits<M>::THREADS, 0, st>>>(s->A, s->p, s->q, g, s->part, s->st,
-                                                                         h, 0);
+        if (s->A.col16)
+            cg_spmv_pq<M, true, int16_t><<<s->grid[0], SpTraits<M>::THREADS, 0, st>>>(s->A, s->p, s->q, g,
+                                                                                      s->part, s->st, h, 0);
+        else
+            cg_spmv_pq<M, true, int32_t><<<s->grid[0], SpTraits<M>::THREADS, 0, st>>>(s->A, s->p, s->q, g,
+                                                                                      s->part, s->st, h, 0);
         break;
     case MWCG_STAGE_FINAL_ALPHA: cg_finalize<M><<<1, TILE_THREADS, 0, st>>>(s->part, g, s->st, 1); break;
     case MWCG_STAGE_UPDATE:
@@ -617,11 +630,13 @@ int compute_grids_t(mwcg_solver *s) {
     MWCG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     int nb[4] = {1, 1, 1, 1};
     if (s->fused) {
-        MWCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb[0], cg_spmv_pq<M, true>, SpTraits<M>::THREADS, 0));
+        MWCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb[0], cg_spmv_pq<M, true, int32_t>,
+                                                                SpTraits<M>::THREADS, 0));
         MWCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb[1], cg_update<M, true>, TILE_THREADS, 0));
         MWCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb[3], cg_init<M, true>, TILE_THREADS, 0));
     } else {
-        MWCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb[0], cg_spmv_pq<M, false>, SpTraits<M>::THREADS, 0));
+        MWCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb[0], cg_spmv_pq<M, false, int32_t>,
+                                                                SpTraits<M>::THREADS, 0));
         MWCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb[1], cg_update<M, false>, TILE_THREADS, 0));
         MWCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb[3], cg_init<M, false>, TILE_THREADS, 0));
     }
@@ -906,11 +921,19 @@ int mwcg_solver_create_dist(mwcg_solver **out, const mwcg_matrix *A, const mwcg_
     return 0;
 }
 
-int mwcg_solver_dist_stage(mwcg_solver *s, int stage) {
+int mwcg_solver_dist_stage(mwcg_solver *s, int stage, void *stream) {
     if (!s || !s->dist) {
         set_error("not a distributed solver");
         return MWCG_ERR_STATE;
     }
+    // launch on the caller's current stream (lets dist.py capture a segment
+    // into a CUDA graph); NULL keeps the solver's stream
+    struct StreamGuard {
+        mwcg_solver *s;
+        cudaStream_t old;
+        ~StreamGuard() { s->stream = old; }
+    } guard{s, s->stream};
+    if (stream) s->stream = (cudaStream_t)stream;
     if (s->n == 0 && (stage == MWCG_STAGE_INIT || stage == MWCG_STAGE_SPMV || stage == MWCG_STAGE_UPDATE ||
                       stage == MWCG_STAGE_XPAY))
         return 0;  // a rank without rows still takes part in the finalize stages
@@ -1034,11 +1057,19 @@ int mwcg_solver_run_profiled(mwcg_solver *s, int64_t k_stop, double *ms) {
         const unsigned pb = (unsigned)((s->parts + 127) / 128);                                            \
         const Geo &g = s->geo;                                                                             \
         if (s->fused) {                                                                                    \
-            cg_spmv_pq<Mx, true><<<s->grid[0], SpTraits<Mx>::THREADS, 0, st>>>(s->A, s->p, s->q, g,        \
-                                                                              s->part, s->st, h, 0);       \
+            if (s->A.col16)                                                                                \
+                cg_spmv_pq<Mx, true, int16_t><<<s->grid[0], SpTraits<Mx>::THREADS, 0, st>>>(               \
+                    s->A, s->p, s->q, g, s->part, s->st, h, 0);                                            \
+            else                                                                                           \
+                cg_spmv_pq<Mx, true, int32_t><<<s->grid[0], SpTraits<Mx>::THREADS, 0, st>>>(               \
+                    s->A, s->p, s->q, g, s->part, s->st, h, 0);                                            \
         } else {                                                                                           \
-            cg_spmv_pq<Mx, false><<<s->grid[0], SpTraits<Mx>::THREADS, 0, st>>>(s->A, s->p, s->q, g,       \
-                                                                               s->part, s->st, h, 0);      \
+            if (s->A.col16)                                                                                \
+                cg_spmv_pq<Mx, false, int16_t><<<s->grid[0], SpTraits<Mx>::THREADS, 0, st>>>(              \
+                    s->A, s->p, s->q, g, s->part, s->st, h, 0);                                            \
+            else                                                                                           \
+                cg_spmv_pq<Mx, false, int32_t><<<s->grid[0], SpTraits<Mx>::THREADS, 0, st>>>(              \
+                    s->A, s->p, s->q, g, s->part, s->st, h, 0);                                            \
             cg_dot_part<Mx><<<pb, 128, 0, st>>>(s->n, s->p, s->q, s->n, s->parts, s->part, s->st, 1);      \
             cg_ref_combine<Mx><<<1, 1, 0, st>>>(s->part, s->parts, s->st, 1, h, 0);                        \
         }                                                                                                  \
@@ -1147,7 +1178,10 @@ int mwcg_solver_metrics(mwcg_solver *s, double *err, double *true_res) {
     case TW: promote_kernel<TW><<<eb, 256, 0, st>>>(n, s->x, n, s->xt); break;
     default: promote_kernel<QTW><<<eb, 256, 0, st>>>(n, s->x, n, s->xt); break;
     }
-    metrics_vec_kernel<<<eb, TILE_THREADS, 0, st>>>(s->A, s->xt, s->b, s->x_star, s->res, s->diff);
+    if (s->A.col16)
+        metrics_vec_kernel<int16_t><<<eb, TILE_THREADS, 0, st>>>(s->A, s->xt, s->b, s->x_star, s->res, s->diff);
+    else
+        metrics_vec_kernel<int32_t><<<eb, TILE_THREADS, 0, st>>>(s->A, s->xt, s->b, s->x_star, s->res, s->diff);
     MWCG_CHECK_LAUNCH();
     if ((rc = tw_sumsq(s, s->res, 0))) return rc;
     if (s->x_star && (rc = tw_sumsq(s, s->diff, 1))) return rc;

@@ -154,20 +154,39 @@ __device__ __forceinline__ mw::V<mw::Arith<M>::W> block_tree_first(mw::V<mw::Ari
     return v;
 }
 
+// Thread t of the reducing block accumulates partials t, t+256, t+512, ...
+// in increasing order (the canonical order).  The loads are issued PF at a
+// time before the dependent additions, so the serial tail of the last block
+// pays one L2 round trip per PF partials instead of one per partial.
+template <int M>
+__device__ __forceinline__ mw::V<mw::Arith<M>::W> accumulate_partials(const double *part, int64_t ld,
+                                                                      int64_t ntiles) {
+    using A = mw::Arith<M>;
+    constexpr int W = A::W;
+    constexpr int PF = 8;
+    mw::V<W> acc = mw::zero<W>();
+    for (int64_t b = threadIdx.x; b < ntiles; b += (int64_t)PF * TILE_THREADS) {
+        mw::V<W> t[PF];
+#pragma unroll
+        for (int j = 0; j < PF; j++) {
+            const int64_t idx = b + (int64_t)j * TILE_THREADS;
+#pragma unroll
+            for (int k = 0; k < W; k++) t[j].w[k] = idx < ntiles ? __ldcg(part + k * ld + idx) : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < PF; j++)
+            if (b + (int64_t)j * TILE_THREADS < ntiles) acc = A::add(acc, t[j]);
+    }
+    return acc;
+}
+
 template <int M>
 __device__ __forceinline__ mw::V<mw::Arith<M>::W> reduce_partials_first(const double *part, int64_t ld,
                                                                          int64_t ntiles, double *smem) {
     using A = mw::Arith<M>;
     constexpr int W = A::W;
     mw::V<W> acc = mw::zero<W>();
-    if (threadIdx.x < TILE_THREADS) {
-        for (int64_t idx = threadIdx.x; idx < ntiles; idx += TILE_THREADS) {
-            mw::V<W> t;
-#pragma unroll
-            for (int k = 0; k < W; k++) t.w[k] = __ldcg(part + k * ld + idx);
-            acc = A::add(acc, t);
-        }
-    }
+    if (threadIdx.x < TILE_THREADS) acc = accumulate_partials<M>(part, ld, ntiles);
     return block_tree_first<M, TILE_THREADS>(acc, smem);
 }
 
@@ -177,16 +196,7 @@ __device__ __forceinline__ mw::V<mw::Arith<M>::W> reduce_partials_first(const do
 template <int M>
 __device__ __forceinline__ mw::V<mw::Arith<M>::W> reduce_partials_block(const double *part, int64_t ld,
                                                                          int64_t ntiles, double *smem) {
-    using A = mw::Arith<M>;
-    constexpr int W = A::W;
-    mw::V<W> acc = mw::zero<W>();
-    for (int64_t idx = threadIdx.x; idx < ntiles; idx += TILE_THREADS) {
-        mw::V<W> t;
-#pragma unroll
-        for (int k = 0; k < W; k++) t.w[k] = __ldcg(part + k * ld + idx);
-        acc = A::add(acc, t);
-    }
-    return block_tree<M, TILE_THREADS>(acc, smem);
+    return block_tree<M, TILE_THREADS>(accumulate_partials<M>(part, ld, ntiles), smem);
 }
 
 // Last-block-done election: returns true in every thread of the block that

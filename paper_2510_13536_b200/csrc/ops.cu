@@ -9,7 +9,7 @@ namespace mwcg {
 
 using namespace mw;
 
-template <int M>
+template <int M, typename CT>
 __global__ void __launch_bounds__(TILE_THREADS) spmv_kernel(SellMatrix A, const double *__restrict__ x,
                                                             int64_t ldx, double *__restrict__ y,
                                                             int64_t ldy) {
@@ -18,7 +18,7 @@ __global__ void __launch_bounds__(TILE_THREADS) spmv_kernel(SellMatrix A, const 
 #pragma unroll 1
     for (int j = 0; j < TILE_ELEMS; j++) {
         int64_t row = base + j * TILE_THREADS;
-        if (row < A.n_rows) store<W>(y, ldy, row, spmv_row<M>(A, x, ldx, row));
+        if (row < A.n_rows) store<W>(y, ldy, row, spmv_row<M, 8, CT>(A, x, ldx, row));
     }
 }
 
@@ -190,7 +190,11 @@ int launch_spmv(int mode, const SellMatrix &A, const double *x, int64_t ldx, dou
                 cudaStream_t st) {
     int64_t tiles = num_tiles(A.n_rows);
     if (tiles == 0) return 0;
-#define L(Mx) spmv_kernel<Mx><<<(unsigned)tiles, TILE_THREADS, 0, st>>>(A, x, ldx, y, ldy)
+#define L(Mx)                                                                                          \
+    do {                                                                                               \
+        if (A.col16) spmv_kernel<Mx, int16_t><<<(unsigned)tiles, TILE_THREADS, 0, st>>>(A, x, ldx, y, ldy); \
+        else spmv_kernel<Mx, int32_t><<<(unsigned)tiles, TILE_THREADS, 0, st>>>(A, x, ldx, y, ldy);         \
+    } while (0)
     MWCG_DISPATCH(mode, L);
 #undef L
     MWCG_CHECK_LAUNCH();

@@ -23,7 +23,20 @@ __device__ __forceinline__ double ld_stream(const double *p) { return __ldcs(p);
 // U column/value loads issue back to back (indices clamped, unconditional),
 // then the U gathers of x, then the dependent arithmetic chain -- two memory
 // round trips per chunk (a 7-point row is one chunk).
-template <int M, int U = 8>
+template <typename CT>
+struct ColCodec;
+template <>
+struct ColCodec<int16_t> {  // int16 delta to the (global) row
+    static constexpr int16_t SENT = COL16_SENT;
+    static __device__ __forceinline__ int col(int grow, int16_t d) { return grow + d; }
+};
+template <>
+struct ColCodec<int32_t> {  // absolute int32 column
+    static constexpr int32_t SENT = COL32_SENT;
+    static __device__ __forceinline__ int col(int, int32_t d) { return d; }
+};
+
+template <int M, int U, typename CT>
 __device__ __forceinline__ mw::V<mw::Arith<M>::W> spmv_row(const SellMatrix &A,
                                                            const double *__restrict__ x, int64_t ldx,
                                                            int64_t row) {
@@ -33,34 +46,22 @@ __device__ __forceinline__ mw::V<mw::Arith<M>::W> spmv_row(const SellMatrix &A,
     const int64_t s0 = __ldg(A.slice_ptr + sl);
     const int L = (int)((__ldg(A.slice_ptr + sl + 1) - s0) >> 5);
     const int64_t off = s0 + (row & 31);
-    const int64_t grow = A.row_base + row;
+    const int grow = (int)(A.row_base + row);  // n_cols < 2^31 (sell.cu)
+    const CT *__restrict__ cp = (const CT *)A.cols + off;
     const double *__restrict__ vp = A.vals + off;
     mw::V<W> s = mw::zero<W>();
     for (int k0 = 0; k0 < L; k0 += U) {
-        int64_t c[U];
+        int c[U];
         bool ok[U];
         double a[U];
-        if (A.col16) {
-            const int16_t *__restrict__ cp = (const int16_t *)A.cols + off;
 #pragma unroll
-            for (int u = 0; u < U; u++) {
-                const int kk = min(k0 + u, L - 1);
-                const int16_t d = ld_stream(cp + (int64_t)kk * SLICE);
-                ok[u] = (k0 + u < L) && (d != COL16_SENT);
-                c[u] = ok[u] ? grow + d : 0;
-            }
-        } else {
-            const int32_t *__restrict__ cp = (const int32_t *)A.cols + off;
-#pragma unroll
-            for (int u = 0; u < U; u++) {
-                const int kk = min(k0 + u, L - 1);
-                const int32_t d = ld_stream(cp + (int64_t)kk * SLICE);
-                ok[u] = (k0 + u < L) && (d != COL32_SENT);
-                c[u] = ok[u] ? d : 0;
-            }
+        for (int u = 0; u < U; u++) {
+            const int64_t kk = min(k0 + u, L - 1);
+            const CT d = ld_stream(cp + kk * SLICE);
+            a[u] = ld_stream(vp + kk * SLICE);
+            ok[u] = (k0 + u < L) && (d != ColCodec<CT>::SENT);
+            c[u] = ok[u] ? ColCodec<CT>::col(grow, d) : 0;
         }
-#pragma unroll
-        for (int u = 0; u < U; u++) a[u] = ld_stream(vp + (int64_t)min(k0 + u, L - 1) * SLICE);
         mw::V<W> xv[U];
 #pragma unroll
         for (int u = 0; u < U; u++) xv[u] = mw::load_ro<W>(x, ldx, c[u]);
@@ -70,5 +71,8 @@ __device__ __forceinline__ mw::V<mw::Arith<M>::W> spmv_row(const SellMatrix &A,
     }
     return s;
 }
+
+// dispatch helper: F<CT>() with the matrix's column type
+#define MWCG_COLS(A, F) ((A).col16 ? F(int16_t) : F(int32_t))
 
 }  // namespace mwcg

@@ -123,7 +123,8 @@ class RankSolver:
                                              int(max_iterations)))
 
     def stage(self, name):
-        _lib.check(self._L.mwcg_solver_dist_stage(self.handle, _lib.STAGE[name]))
+        _lib.check(self._L.mwcg_solver_dist_stage(self.handle, _lib.STAGE[name],
+                                                  _lib.stream_handle()))
 
     def state(self):
         s = _lib.StateC()
@@ -183,31 +184,60 @@ class DistResult:
     final_recurrence_residual: float
 
 
+def _iteration(ranks, exchange):
+    for rs in ranks:
+        rs.stage("spmv")
+    exchange.gather(ranks, "part")
+    for rs in ranks:
+        rs.stage("final_alpha")
+    for rs in ranks:
+        rs.stage("update")
+    exchange.gather(ranks, "part")
+    for rs in ranks:
+        rs.stage("final_beta")
+    for rs in ranks:
+        rs.stage("xpay")
+    exchange.gather(ranks, "p")
+
+
 def dist_cg_solve(ranks, exchange, b_norm, epsilon=1e-12, max_iterations=None,
-                  check_every=16):
-    """Drive the SPMD stages over `ranks` (all local ranks of this process)."""
+                  check_every=16, graph=False):
+    """Drive the SPMD stages over `ranks` (all local ranks of this process).
+
+    graph=True captures `check_every` iterations -- stage kernels and the
+    NCCL all-gathers -- into one CUDA graph and replays it, so the host does
+    one launch per segment instead of ~10 per iteration.  Stages after the
+    stop test early-exit on the device status; the segment's remaining
+    exchanges are harmless."""
     part = ranks[0].part
-    max_it = int(max_iterations if max_iterations is not None else 10 * part.n)
     exchange.gather(ranks, "part")
     for rs in ranks:
         rs.stage("final_init")
     exchange.gather(ranks, "p")
     st = ranks[0].state()
-    while st.status == 0:
+    g = None
+    if graph and st.status == 0:
+        # one eager segment first (NCCL communicators / lazy init), then capture
         for _ in range(check_every):
-            for rs in ranks:
-                rs.stage("spmv")
-            exchange.gather(ranks, "part")
-            for rs in ranks:
-                rs.stage("final_alpha")
-            for rs in ranks:
-                rs.stage("update")
-            exchange.gather(ranks, "part")
-            for rs in ranks:
-                rs.stage("final_beta")
-            for rs in ranks:
-                rs.stage("xpay")
-            exchange.gather(ranks, "p")
+            _iteration(ranks, exchange)
+        st = ranks[0].state()
+        if st.status == 0:
+            try:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    for _ in range(check_every):
+                        _iteration(ranks, exchange)
+                g.replay()   # the captured segment is not executed by capture itself
+            except Exception:  # pragma: no cover - capture unsupported: stay eager
+                g = None
+                torch.cuda.synchronize()
+            st = ranks[0].state()
+    while st.status == 0:
+        if g is not None:
+            g.replay()
+        else:
+            for _ in range(check_every):
+                _iteration(ranks, exchange)
         st = ranks[0].state()
     reason = _lib.STATUS[st.status]
     return DistResult(reason == "converged", reason, int(st.iterations), float(st.rel))
@@ -215,7 +245,7 @@ def dist_cg_solve(ranks, exchange, b_norm, epsilon=1e-12, max_iterations=None,
 
 def solve_partitioned(A, b, world, mode="dw", epsilon=1e-12, max_iterations=None, x0=None,
                       normalization="after-axpy", exchange=None, ranks_here=None,
-                      check_every=16):
+                      check_every=16, graph=False):
     """Convenience: build the rank solvers for `ranks_here` (default: all
     ranks, emulated in this process) and solve.  Returns (result, x words of
     the local ranks concatenated)."""
@@ -238,6 +268,6 @@ def solve_partitioned(A, b, world, mode="dw", epsilon=1e-12, max_iterations=None
         rs.start(b_loc, _b_norm(b), x0_full, epsilon, max_iterations if max_iterations is not None
                  else 10 * A.n_rows)
         ranks.append(rs)
-    res = dist_cg_solve(ranks, exchange, _b_norm(b), epsilon, max_iterations, check_every)
+    res = dist_cg_solve(ranks, exchange, _b_norm(b), epsilon, max_iterations, check_every, graph)
     x = torch.cat([rs.solution() for rs in ranks], dim=1)
     return res, x

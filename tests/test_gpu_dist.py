@@ -54,3 +54,16 @@ def test_partition_geometry():
     assert [p.rows(r) for r in range(3)] == [(0, 4096), (4096, 8192), (8192, 10000)]
     p8 = partition(10_000, 8)
     assert p8.rows(7) == (10_000, 10_000)
+
+
+@pytest.mark.parametrize("mode", ["dw", "qtw"])
+def test_partitioned_graph_replay_equals_eager(mode):
+    """The CUDA-graph segment replay (stage kernels + exchanges captured)
+    gives the same bits as the eager driver and as one GPU."""
+    A = laplacian_2d(100)
+    xs = np.random.default_rng(4).uniform(-1, 1, A.n_rows)
+    b = problems.spmv_fp64_host(A, xs)
+    single = cg.cg_solve(A, b, cg.SolverConfig(mode=mode, epsilon=1e-20, history_stride=10**6))
+    res, x = solve_partitioned(A, b, 3, mode=mode, epsilon=1e-20, check_every=8, graph=True)
+    assert res.iterations == single.iterations
+    assert np.array_equal(_bits(x), _bits(single.x.planes))
