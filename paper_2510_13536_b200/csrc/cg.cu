@@ -150,18 +150,18 @@ struct SpTraits {
 #ifdef MWCG_SP_THREADS_OVERRIDE
     static constexpr int THREADS = MWCG_SP_THREADS_OVERRIDE;
 #else
-    static constexpr int THREADS = (M == TW || M == QTW) ? 256 : 512;
+    static constexpr int THREADS = (M == FP64) ? 512 : 256;
 #endif
 #ifdef MWCG_SP_MINB_OVERRIDE
     static constexpr int MINB = MWCG_SP_MINB_OVERRIDE;
 #else
-    static constexpr int MINB = (M == FP64) ? 3 : ((M == TW || M == QTW) ? 4 : 2);
+    static constexpr int MINB = (M == FP64) ? 3 : ((M == TW || M == QTW) ? 4 : 5);
 #endif
     static constexpr int RPT = TILE / THREADS;
 #ifdef MWCG_SP_U_OVERRIDE
     static constexpr int U = MWCG_SP_U_OVERRIDE;
 #else
-    static constexpr int U = (M == TW || M == QTW) ? 4 : 8;
+    static constexpr int U = (M == FP64) ? 8 : 4;
 #endif
 };
 
