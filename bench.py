@@ -47,7 +47,7 @@ FLOPS = {"fp64": (2, 10), "dw": (17, 90), "qdw": (11, 63), "tw": (96, 540), "qtw
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4"])
