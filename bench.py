@@ -392,7 +392,7 @@ def run_ours(a):
             object.__setattr__(Ah, "values", pin["va"].numpy())
             object.__setattr__(Ah, "_device", None)
             r = cg.cg_solve(Ah, pin["b"].numpy(), conf)
-            xw = r.x.planes.cpu()  # solution words back to the host
+            xw = r.x.to_host()  # solution words back to the host (pinned)
             return r, xw
 
         CsrMatrix(n, n, A.row_ptr, A.col_idx, A.values)  # validation (not timed)

@@ -95,7 +95,7 @@ class SolverResult:
 
 def _dev_f64(a):
     t = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64))
-    return t.to("cuda", non_blocking=False)
+    return t.to("cuda", non_blocking=True)
 
 
 class Solver:

@@ -701,7 +701,7 @@ void free_solver(mwcg_solver *s) {
     pool_free(s->mpart, st);
     pool_free(s->mout, st);
     pool_free(s->mticket, st);
-    if (s->st_host) cudaFreeHost(s->st_host);
+    delete[] reinterpret_cast<double *>(s->st_host);
     for (auto &e : s->ev)
         if (e) cudaEventDestroy(e);
     if (s->cap) cudaStreamDestroy(s->cap);
@@ -830,7 +830,10 @@ int mwcg_solver_create(mwcg_solver **out, const mwcg_matrix *A, const mwcg_solve
     TRY(pool_alloc((void **)&s->st, sizeof(CgState), s->stream));
     TRY(cudaMemsetAsync(s->st, 0, sizeof(CgState), s->stream));
     // one pinned block for the host mirrors: state, k_stop, metric sums
-    TRY(cudaMallocHost((void **)&s->st_host, sizeof(CgState) + 16 * sizeof(double)));
+    // host mirrors in pageable memory: every D2H of the state is followed by a
+    // stream sync anyway, and pinned alloc/free (cudaFreeHost synchronizes the
+    // device) would dominate short solves that create and drop solvers
+    s->st_host = (CgState *)new double[(sizeof(CgState) + 16 * sizeof(double) + 7) / 8];
     s->kstop_host = (long long *)((char *)s->st_host + sizeof(CgState));
     s->mout_host = (double *)((char *)s->st_host + sizeof(CgState) + 2 * sizeof(double));
     TRY(cudaStreamCreateWithFlags(&s->cap, cudaStreamNonBlocking));
@@ -903,7 +906,10 @@ int mwcg_solver_create_dist(mwcg_solver **out, const mwcg_matrix *A, const mwcg_
     TRY(pool_alloc((void **)&s->q, vbytes, s->stream));
     TRY(pool_alloc((void **)&s->st, sizeof(CgState), s->stream));
     TRY(cudaMemsetAsync(s->st, 0, sizeof(CgState), s->stream));
-    TRY(cudaMallocHost((void **)&s->st_host, sizeof(CgState) + 16 * sizeof(double)));
+    // host mirrors in pageable memory: every D2H of the state is followed by a
+    // stream sync anyway, and pinned alloc/free (cudaFreeHost synchronizes the
+    // device) would dominate short solves that create and drop solvers
+    s->st_host = (CgState *)new double[(sizeof(CgState) + 16 * sizeof(double) + 7) / 8];
     s->kstop_host = (long long *)((char *)s->st_host + sizeof(CgState));
     s->mout_host = (double *)((char *)s->st_host + sizeof(CgState) + 2 * sizeof(double));
     for (auto &e : s->ev) TRY(cudaEventCreate(&e));

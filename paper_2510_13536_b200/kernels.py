@@ -66,10 +66,17 @@ class MultiwordVector:
             t = t.reshape(1, -1)
         return cls(mode, t.shape[1], t)
 
+    def to_host(self):
+        """(w, n) host copy of the word planes through a pinned buffer."""
+        h = torch.empty(tuple(self.planes.shape), dtype=torch.float64, pin_memory=True)
+        h.copy_(self.planes, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return h.numpy()
+
     @property
     def words(self):
         """Host snapshot of the word planes, w0 highest (kernels.py:69-74)."""
-        h = self.planes.cpu().numpy()
+        h = self.to_host()
         return tuple(h[k] for k in range(h.shape[0]))
 
     def __len__(self):
@@ -114,9 +121,11 @@ def device_matrix(A, row_base=0, col_format=-1):
         return h
     L = _lib.load()
     dev = _cuda()
-    rp = torch.from_numpy(np.ascontiguousarray(A.row_ptr, dtype=np.int64)).to(dev)
-    ci = torch.from_numpy(np.ascontiguousarray(A.col_idx, dtype=np.int64)).to(dev)
-    va = torch.from_numpy(np.ascontiguousarray(A.values, dtype=np.float64)).to(dev)
+    # non_blocking: a DMA straight from the caller's buffers when they are
+    # pinned (torch checks); pageable buffers fall back to a staged copy
+    rp = torch.from_numpy(np.ascontiguousarray(A.row_ptr, dtype=np.int64)).to(dev, non_blocking=True)
+    ci = torch.from_numpy(np.ascontiguousarray(A.col_idx, dtype=np.int64)).to(dev, non_blocking=True)
+    va = torch.from_numpy(np.ascontiguousarray(A.values, dtype=np.float64)).to(dev, non_blocking=True)
     handle = ctypes.c_void_p()
     _lib.check(L.mwcg_matrix_create_ex(ctypes.byref(handle), A.n_rows, A.n_cols, A.nnz,
                                        _lib.ptr(rp), _lib.ptr(ci), _lib.ptr(va), 8, int(row_base),

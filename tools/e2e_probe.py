@@ -25,7 +25,7 @@ for it in range(4):
     sv = cg.Solver(Ah, "dw"); torch.cuda.synchronize(); t2 = time.perf_counter()
     object.__setattr__(Ah, "_solvers", {("dw", "after-axpy", "tile", 1): sv})
     r = cg.cg_solve(Ah, pin["b"].numpy(), conf); t3 = time.perf_counter()
-    xw = r.x.planes.cpu(); t4 = time.perf_counter()
+    xw = r.x.to_host(); t4 = time.perf_counter()
     print(f"step {it}: matrix {1e3*(t1-t0):.1f} ms  solver(graph) {1e3*(t2-t1):.1f} ms  "
           f"cg_solve {1e3*(t3-t2):.1f} ms (device loop {1e3*r.device_seconds:.1f}, hist {1e3*r.history_seconds:.1f})  "
           f"x->host {1e3*(t4-t3):.1f} ms", flush=True)
