@@ -127,6 +127,9 @@ __device__ __forceinline__ int64_t snake(int64_t t, int64_t ntiles, int dir) {
 // partition: local rows / tiles, p a full replica (ldp =
 // padded global length) with the local slice at p_off, partials written at
 // global tile indices, final_ = 0 (reduced by cg_finalize after the gather).
+// The search direction p is stored INTERLEAVED (AoS, record = W words): it is
+// the gathered vector, and one record per gather halves (DW) / thirds (TW)
+// the sectors a random column costs; x, r, q stay in SoA word planes.
 struct Geo {
     int64_t n, ld, ldp, p_off;
     int64_t ntiles, tile_off, part_ld, ntiles_glob;
@@ -189,10 +192,10 @@ __global__ void __launch_bounds__(SpTraits<M>::THREADS, SpTraits<M>::MINB)
             V<W> term = zero<W>();
             if (row < n) {
                 // columns are global: p is the full (replicated) vector
-                V<W> sv = spmv_row<M, SpTraits<M>::U, CT>(A, p, g.ldp, row);
+                V<W> sv = spmv_row<M, SpTraits<M>::U, CT, true>(A, p, 0, row);
                 if (norm_all) sv = Ar::norm(sv);
                 store<W>(q, g.ld, row, sv);
-                if (FUSED) term = Ar::mul(load_ro<W>(p, g.ldp, g.p_off + row), sv);
+                if (FUSED) term = Ar::mul(load_aos_ro<W>(p, g.p_off + row), sv);
             }
             if (FUSED) {
 #pragma unroll
@@ -266,8 +269,8 @@ __global__ void __launch_bounds__(TILE_THREADS, Hoist<M>::MINB)
         alpha.w[k] = st->alpha[k];
         nalpha.w[k] = st->neg_alpha[k];
     }
-    const int64_t n = g.n, ld = g.ld, ldp = g.ldp;
-    const double *__restrict__ pl = p + g.p_off;  // local slice of p
+    const int64_t n = g.n, ld = g.ld;
+    const double *__restrict__ pl = p + g.p_off * W;  // local slice of p (AoS)
     const int dir = (int)((st->k & 1) ^ 1);
     for (int64_t t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
         const int64_t tile = snake(t, g.ntiles, dir);
@@ -281,7 +284,7 @@ __global__ void __launch_bounds__(TILE_THREADS, Hoist<M>::MINB)
                 int64_t i = base + (j0 + h2) * TILE_THREADS;
                 if (i < n) {
                     xv[h2] = load<W>(x, ld, i);
-                    pv[h2] = load_ro<W>(pl, ldp, i);
+                    pv[h2] = load_aos_ro<W>(pl, i);
                     rv[h2] = load<W>(r, ld, i);
                     qv[h2] = load_ro<W>(q, ld, i);
                 }
@@ -326,8 +329,8 @@ __global__ void __launch_bounds__(TILE_THREADS)
     V<W> beta;
 #pragma unroll
     for (int k = 0; k < W; k++) beta.w[k] = st->beta[k];
-    const int64_t n = g.n, ld = g.ld, ldp = g.ldp;
-    double *__restrict__ pl = p + g.p_off;
+    const int64_t n = g.n, ld = g.ld;
+    double *__restrict__ pl = p + g.p_off * W;
     const int dir = (int)((st->k & 1) ^ 1);
     for (int64_t t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
         const int64_t tile = snake(t, g.ntiles, dir);
@@ -338,7 +341,7 @@ __global__ void __launch_bounds__(TILE_THREADS)
             int64_t i = base + j * TILE_THREADS;
             if (i < n) {
                 rv[j] = load_ro<W>(r, ld, i);
-                pv[j] = load<W>(pl, ldp, i);
+                pv[j] = load_aos<W>(pl, i);
             }
         }
 #pragma unroll
@@ -347,7 +350,7 @@ __global__ void __launch_bounds__(TILE_THREADS)
             if (i < n) {
                 V<W> pi = Ar::add(rv[j], Ar::mul(beta, pv[j]));
                 if (norm_all) pi = Ar::norm(pi);
-                store<W>(pl, ldp, i, pi);
+                store_aos<W>(pl, i, pi);
             }
         }
     }
@@ -365,8 +368,8 @@ __global__ void __launch_bounds__(TILE_THREADS)
     __shared__ double smem[W * TILE_THREADS / 32];
     __shared__ int s_last;
     const bool norm_r = st->norm_r != 0;
-    const int64_t n = g.n, ld = g.ld, ldp = g.ldp;
-    double *__restrict__ pl = p + g.p_off;
+    const int64_t n = g.n, ld = g.ld;
+    double *__restrict__ pl = p + g.p_off * W;
     for (int64_t tile = blockIdx.x; tile < g.ntiles; tile += gridDim.x) {
         const int64_t base = tile * TILE + threadIdx.x;
         V<W> acc = zero<W>();
@@ -377,7 +380,7 @@ __global__ void __launch_bounds__(TILE_THREADS)
                 V<W> ri = Ar::dxadd(b[i], neg<W>(load<W>(q, ld, i)));
                 if (norm_r) ri = Ar::norm(ri);
                 store<W>(r, ld, i, ri);
-                store<W>(pl, ldp, i, ri);
+                store_aos<W>(pl, i, ri);
                 if (FUSED) acc = Ar::add(acc, Ar::mul(ri, ri));
             }
         }
@@ -393,6 +396,28 @@ __global__ void __launch_bounds__(TILE_THREADS)
         st->ticket[2] = 0u;
         scalar_init<M>(st, rho);
     }
+}
+
+// ---------------------------------------------------------------- dist start
+// p (AoS, full replica) <- x0 word 0; q = A p for the local rows (no
+// normalisation: cg.py:113 applies none to the initial q)
+template <int W>
+__global__ void spread_x0_kernel(int64_t n, const double *__restrict__ x0, double *__restrict__ p) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        V<W> v = zero<W>();
+        v.w[0] = x0 ? x0[i] : 0.0;
+        store_aos<W>(p, i, v);
+    }
+}
+
+template <int M, typename CT>
+__global__ void __launch_bounds__(TILE_THREADS)
+    spmv_aos_kernel(SellMatrix A, const double *__restrict__ p, double *__restrict__ q, int64_t ldq) {
+    constexpr int W = Arith<M>::W;
+    for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < A.n_rows;
+         row += (int64_t)gridDim.x * blockDim.x)
+        store<W>(q, ldq, row, spmv_row<M, 8, CT, true>(A, p, 0, row));
 }
 
 // ---------------------------------------------------------------- finalize (multi-rank)
@@ -417,7 +442,7 @@ __global__ void __launch_bounds__(TILE_THREADS)
 }
 
 // ---------------------------------------------------------------- reference-order dots
-template <int M>
+template <int M, bool XAOS>
 __global__ void cg_dot_part(int64_t n, const double *__restrict__ x, const double *__restrict__ y,
                             int64_t ld, int64_t parts, double *__restrict__ part, const CgState *st,
                             int check_status) {
@@ -429,7 +454,8 @@ __global__ void cg_dot_part(int64_t n, const double *__restrict__ x, const doubl
     int64_t lo = (int64_t)(((__int128)n * pidx) / parts);
     int64_t hi = (int64_t)(((__int128)n * (pidx + 1)) / parts);
     V<W> t = zero<W>();
-    for (int64_t i = lo; i < hi; i++) t = Ar::add(t, Ar::mul(load<W>(x, ld, i), load<W>(y, ld, i)));
+    for (int64_t i = lo; i < hi; i++)
+        t = Ar::add(t, Ar::mul(XAOS ? load_aos<W>(x, i) : load<W>(x, ld, i), load<W>(y, ld, i)));
     store<W>(part, parts, pidx, t);
 }
 
@@ -552,11 +578,11 @@ int enqueue_iteration(mwcg_solver *s, cudaStream_t st, cudaGraphConditionalHandl
         else
             cg_spmv_pq<M, false, int32_t><<<g0, SpTraits<M>::THREADS, 0, st>>>(s->A, s->p, s->q, g, s->part,
                                                                                s->st, h, use_cond);
-        cg_dot_part<M><<<pb, 128, 0, st>>>(s->n, s->p, s->q, s->n, s->parts, s->part, s->st, 1);
+        cg_dot_part<M, true><<<pb, 128, 0, st>>>(s->n, s->p, s->q, s->n, s->parts, s->part, s->st, 1);
         cg_ref_combine<M><<<1, 1, 0, st>>>(s->part, s->parts, s->st, 1, h, use_cond);
         cg_update<M, false><<<g1, TILE_THREADS, 0, st>>>(s->x, s->r, s->p, s->q, g, s->part, s->st, h,
                                                           use_cond);
-        cg_dot_part<M><<<pb, 128, 0, st>>>(s->n, s->r, s->r, s->n, s->parts, s->part, s->st, 1);
+        cg_dot_part<M, false><<<pb, 128, 0, st>>>(s->n, s->r, s->r, s->n, s->parts, s->part, s->st, 1);
         cg_ref_combine<M><<<1, 1, 0, st>>>(s->part, s->parts, s->st, 2, h, use_cond);
     }
     cg_xpay<M><<<g2, TILE_THREADS, 0, st>>>(s->p, s->r, g, s->st, h, use_cond);
@@ -584,7 +610,7 @@ int enqueue_init(mwcg_solver *s) {
     } else {
         const unsigned pb = (unsigned)((s->parts + 127) / 128);
         cg_init<M, false><<<tiles, TILE_THREADS, 0, st>>>(s->b, s->q, s->r, s->p, g, s->part, s->st);
-        cg_dot_part<M><<<pb, 128, 0, st>>>(s->n, s->r, s->r, s->n, s->parts, s->part, s->st, 0);
+        cg_dot_part<M, false><<<pb, 128, 0, st>>>(s->n, s->r, s->r, s->n, s->parts, s->part, s->st, 0);
         cg_ref_combine<M><<<1, 1, 0, st>>>(s->part, s->parts, s->st, 0, cudaGraphConditionalHandle{}, 0);
     }
     MWCG_CHECK_LAUNCH();
@@ -994,17 +1020,28 @@ int mwcg_solver_start(mwcg_solver *s, const double *b, double b_norm, const doub
         rc = launch_spmv(s->mode, s->A, s->x, s->n, s->q, s->n, st);
     } else {
         // x0 is the FULL (global, padded) initial guess on every rank: the
-        // local slice seeds x; the SpMV reads the replica through p's buffer
-        // (p is overwritten by the init stage right after).
+        // local slice seeds x; the SpMV reads it through p's buffer (AoS),
+        // which the init stage overwrites right after.
         const int64_t ldp = s->geo.ldp;
-        MWCG_CUDA(cudaMemsetAsync(s->p, 0, sizeof(double) * (size_t)s->W * (size_t)ldp, st));
-        if (x0) {
-            MWCG_CUDA(cudaMemcpyAsync(s->x, x0 + s->geo.p_off, sizeof(double) * (size_t)s->n,
-                                      cudaMemcpyDeviceToDevice, st));
-            MWCG_CUDA(cudaMemcpyAsync(s->p, x0, sizeof(double) * (size_t)ldp, cudaMemcpyDeviceToDevice, st));
+        if (x0) MWCG_CUDA(cudaMemcpyAsync(s->x, x0 + s->geo.p_off, sizeof(double) * (size_t)s->n,
+                                          cudaMemcpyDeviceToDevice, st));
+        const unsigned eb = (unsigned)std::max<int64_t>(1, std::min<int64_t>((ldp + 255) / 256, 148 * 16));
+        const unsigned sb = (unsigned)std::max<int64_t>(1, std::min<int64_t>((s->n + 255) / 256, 148 * 16));
+#define START(Mx)                                                                                    \
+    do {                                                                                             \
+        spread_x0_kernel<words_of(Mx)><<<eb, 256, 0, st>>>(ldp, x0, s->p);                          \
+        if (s->A.col16) spmv_aos_kernel<Mx, int16_t><<<sb, TILE_THREADS, 0, st>>>(s->A, s->p, s->q, s->n); \
+        else spmv_aos_kernel<Mx, int32_t><<<sb, TILE_THREADS, 0, st>>>(s->A, s->p, s->q, s->n);          \
+    } while (0)
+        switch (s->mode) {
+        case FP64: START(FP64); break;
+        case DW: START(DW); break;
+        case QDW: START(QDW); break;
+        case TW: START(TW); break;
+        default: START(QTW); break;
         }
-        rc = launch_spmv(s->mode, s->A, s->p, ldp, s->q, s->n, st);
-        if (rc) return rc;
+#undef START
+        MWCG_CHECK_LAUNCH();
         switch (s->mode) {  // local init stage only; dist.py gathers + finalizes
         case FP64: return enqueue_dist_stage<FP64>(s, MWCG_STAGE_INIT);
         case DW: return enqueue_dist_stage<DW>(s, MWCG_STAGE_INIT);
@@ -1076,7 +1113,7 @@ int mwcg_solver_run_profiled(mwcg_solver *s, int64_t k_stop, double *ms) {
             else                                                                                           \
                 cg_spmv_pq<Mx, false, int32_t><<<s->grid[0], SpTraits<Mx>::THREADS, 0, st>>>(              \
                     s->A, s->p, s->q, g, s->part, s->st, h, 0);                                            \
-            cg_dot_part<Mx><<<pb, 128, 0, st>>>(s->n, s->p, s->q, s->n, s->parts, s->part, s->st, 1);      \
+            cg_dot_part<Mx, true><<<pb, 128, 0, st>>>(s->n, s->p, s->q, s->n, s->parts, s->part, s->st, 1);      \
             cg_ref_combine<Mx><<<1, 1, 0, st>>>(s->part, s->parts, s->st, 1, h, 0);                        \
         }                                                                                                  \
         cudaEventRecord(s->ev[1], st);                                                                     \
@@ -1086,7 +1123,7 @@ int mwcg_solver_run_profiled(mwcg_solver *s, int64_t k_stop, double *ms) {
         } else {                                                                                           \
             cg_update<Mx, false><<<s->grid[1], TILE_THREADS, 0, st>>>(s->x, s->r, s->p, s->q, g, s->part,  \
                                                                        s->st, h, 0);                       \
-            cg_dot_part<Mx><<<pb, 128, 0, st>>>(s->n, s->r, s->r, s->n, s->parts, s->part, s->st, 1);      \
+            cg_dot_part<Mx, false><<<pb, 128, 0, st>>>(s->n, s->r, s->r, s->n, s->parts, s->part, s->st, 1);      \
             cg_ref_combine<Mx><<<1, 1, 0, st>>>(s->part, s->parts, s->st, 2, h, 0);                        \
         }                                                                                                  \
         cudaEventRecord(s->ev[2], st);                                                                     \

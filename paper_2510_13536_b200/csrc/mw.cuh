@@ -450,6 +450,45 @@ MWI void store(double *__restrict__ v, int64_t ld, int64_t i, V<W> a) {
 #pragma unroll
     for (int k = 0; k < W; k++) v[k * ld + i] = a.w[k];
 }
+// Interleaved (AoS) records: word k of element i at v[i*W + k].  The solver
+// stores the search direction p this way: a gather of p[c] is one 8/16/24-B
+// record instead of W loads in W different word planes (sectors).
+template <int W>
+MWI V<W> load_aos(const double *__restrict__ v, int64_t i) {
+    V<W> r;
+    if (W == 2) {
+        const double2 t = *reinterpret_cast<const double2 *>(v + 2 * i);
+        r.w[0] = t.x;
+        r.w[W - 1] = t.y;
+    } else {
+#pragma unroll
+        for (int k = 0; k < W; k++) r.w[k] = v[i * W + k];
+    }
+    return r;
+}
+template <int W>
+MWI V<W> load_aos_ro(const double *__restrict__ v, int64_t i) {
+    V<W> r;
+    if (W == 2) {
+        const double2 t = __ldg(reinterpret_cast<const double2 *>(v + 2 * i));
+        r.w[0] = t.x;
+        r.w[W - 1] = t.y;
+    } else {
+#pragma unroll
+        for (int k = 0; k < W; k++) r.w[k] = __ldg(v + i * W + k);
+    }
+    return r;
+}
+template <int W>
+MWI void store_aos(double *__restrict__ v, int64_t i, V<W> a) {
+    if (W == 2) {
+        *reinterpret_cast<double2 *>(v + 2 * i) = make_double2(a.w[0], a.w[W - 1]);
+    } else {
+#pragma unroll
+        for (int k = 0; k < W; k++) v[i * W + k] = a.w[k];
+    }
+}
+
 template <int W>
 MWI V<W> shfl_down(V<W> a, int off) {
     V<W> r;

@@ -36,7 +36,7 @@ struct ColCodec<int32_t> {  // absolute int32 column
     static __device__ __forceinline__ int col(int, int32_t d) { return d; }
 };
 
-template <int M, int U, typename CT>
+template <int M, int U, typename CT, bool XAOS = false>
 __device__ __forceinline__ mw::V<mw::Arith<M>::W> spmv_row(const SellMatrix &A,
                                                            const double *__restrict__ x, int64_t ldx,
                                                            int64_t row) {
@@ -64,7 +64,8 @@ __device__ __forceinline__ mw::V<mw::Arith<M>::W> spmv_row(const SellMatrix &A,
         }
         mw::V<W> xv[U];
 #pragma unroll
-        for (int u = 0; u < U; u++) xv[u] = mw::load_ro<W>(x, ldx, c[u]);
+        for (int u = 0; u < U; u++)
+            xv[u] = XAOS ? mw::load_aos_ro<W>(x, c[u]) : mw::load_ro<W>(x, ldx, c[u]);
 #pragma unroll
         for (int u = 0; u < U; u++)
             if (ok[u]) s = Ar::add(s, Ar::dxmul(a[u], xv[u]));

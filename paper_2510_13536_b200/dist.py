@@ -6,8 +6,9 @@ ntiles)), i.e. global rows [r*tmax*TILE, ...).  Each rank keeps
 
   * its rows of A (SELL-32 on its GPU) with GLOBAL column indices,
   * x, r, q for its rows,
-  * a full replica of p, shape (w, R*tmax*TILE): the local slice is written by
-    XPAY and the replica is refreshed by an all-gather of the slices,
+  * a full replica of p, shape (R*tmax*TILE, w) -- interleaved words, the
+    layout the kernels gather from: the local slice is written by XPAY and the
+    replica is refreshed by ONE all-gather of the contiguous slices,
   * the tile partials of ALL ranks, shape (w, R*tmax): every rank writes its
     own tiles and an all-gather completes the array.
 
@@ -92,7 +93,7 @@ class RankSolver:
         self.n = self.hi - self.lo
         assert A_local.n_rows == self.n
         self.x = torch.zeros((w, max(self.n, 1)), dtype=torch.float64, device=dev)
-        self.p_full = torch.zeros((w, part.ld_full), dtype=torch.float64, device=dev)
+        self.p_full = torch.zeros((part.ld_full, w), dtype=torch.float64, device=dev)  # AoS
         self.partials = torch.zeros((w, part.part_ld), dtype=torch.float64, device=dev)
         self.dm = device_matrix(A_local, row_base=self.lo)
         L = _lib.load()
@@ -114,6 +115,16 @@ class RankSolver:
 
     def part_slice(self):
         return self.rank * self.part.tmax, self.part.tmax
+
+    def segments(self, which):
+        """1-D (buffer, offset, count) triples this rank contributes to a
+        gather: the AoS p replica is one contiguous block; the SoA tile
+        partials are one block per word plane."""
+        if which == "p":
+            off, cnt = self.p_slice()
+            return [(self.p_full.view(-1), off * self.w, cnt * self.w)]
+        off, cnt = self.part_slice()
+        return [(self.partials[k], off, cnt) for k in range(self.w)]
 
     def start(self, b_local, b_norm, x0_full, epsilon, max_iterations):
         self._b = b_local          # keep alive: the device state points at it
@@ -140,12 +151,11 @@ class LocalExchange:
 
     def gather(self, ranks, which):
         for src in ranks:
-            buf = src.p_full if which == "p" else src.partials
-            off, cnt = src.p_slice() if which == "p" else src.part_slice()
-            seg = buf[:, off:off + cnt]
-            for dst in ranks:
-                if dst is not src:
-                    (dst.p_full if which == "p" else dst.partials)[:, off:off + cnt].copy_(seg)
+            for j, (buf, off, cnt) in enumerate(src.segments(which)):
+                seg = buf[off:off + cnt]
+                for dst in ranks:
+                    if dst is not src:
+                        dst.segments(which)[j][0][off:off + cnt].copy_(seg)
 
 
 class TorchDistExchange:
@@ -160,18 +170,13 @@ class TorchDistExchange:
 
     def gather(self, ranks, which):
         (me,) = ranks
-        buf = me.p_full if which == "p" else me.partials
-        off, cnt = me.p_slice() if which == "p" else me.part_slice()
-        for k in range(buf.shape[0]):
-            plane = buf[k]
-            if self.nccl:
-                self.dist.all_gather_into_tensor(plane, plane[off:off + cnt], group=self.group)
+        for buf, off, cnt in me.segments(which):
+            if self.nccl:  # in-place: each rank's slice already sits at off = rank*cnt
+                self.dist.all_gather_into_tensor(buf, buf[off:off + cnt], group=self.group)
             else:
-                world = buf.shape[1] // cnt
-                outs = list(plane.split(cnt))
-                assert len(outs) == world
+                outs = list(buf.split(cnt))
                 tmp = [torch.empty_like(o) for o in outs]
-                self.dist.all_gather(tmp, plane[off:off + cnt].clone(), group=self.group)
+                self.dist.all_gather(tmp, buf[off:off + cnt].clone(), group=self.group)
                 for o, t in zip(outs, tmp):
                     o.copy_(t)
 

@@ -121,14 +121,19 @@ def device_matrix(A, row_base=0, col_format=-1):
         return h
     L = _lib.load()
     dev = _cuda()
-    # non_blocking: a DMA straight from the caller's buffers when they are
-    # pinned (torch checks); pageable buffers fall back to a staged copy
-    rp = torch.from_numpy(np.ascontiguousarray(A.row_ptr, dtype=np.int64)).to(dev, non_blocking=True)
-    ci = torch.from_numpy(np.ascontiguousarray(A.col_idx, dtype=np.int64)).to(dev, non_blocking=True)
-    va = torch.from_numpy(np.ascontiguousarray(A.values, dtype=np.float64)).to(dev, non_blocking=True)
+    if isinstance(A.row_ptr, torch.Tensor):  # DeviceCsrMatrix: arrays already on the GPU
+        rp, ci, va = A.row_ptr, A.col_idx, A.values
+        ib = rp.element_size()
+    else:
+        # non_blocking: a DMA straight from the caller's buffers when they are
+        # pinned (torch checks); pageable buffers fall back to a staged copy
+        rp = torch.from_numpy(np.ascontiguousarray(A.row_ptr, dtype=np.int64)).to(dev, non_blocking=True)
+        ci = torch.from_numpy(np.ascontiguousarray(A.col_idx, dtype=np.int64)).to(dev, non_blocking=True)
+        va = torch.from_numpy(np.ascontiguousarray(A.values, dtype=np.float64)).to(dev, non_blocking=True)
+        ib = 8
     handle = ctypes.c_void_p()
     _lib.check(L.mwcg_matrix_create_ex(ctypes.byref(handle), A.n_rows, A.n_cols, A.nnz,
-                                       _lib.ptr(rp), _lib.ptr(ci), _lib.ptr(va), 8, int(row_base),
+                                       _lib.ptr(rp), _lib.ptr(ci), _lib.ptr(va), ib, int(row_base),
                                        int(col_format), _lib.stream_handle()))
     dm = _DeviceMatrix(handle, A.n_rows, A.n_cols, A.nnz)
     try:

@@ -154,4 +154,105 @@ def config4(n=1_000_000, half_band=9, delta=1e-3, seed=2):
     return dict(name="C4", A=A, b=b, x_star=ones, epsilon=1e-10, max_iterations=200000)
 
 
-CONFIGS = {"C1": config1, "C2": config2, "C3": config3, "C4": config4}
+def random_irregular_spd(n, seed=3, device="cuda", near_width=1024, cmin=16, cmax=64):
+    """BASELINE config 5 generator, on the GPU (torch, seeded Philox).
+
+    Row i draws c ~ U{cmin..cmax} off-diagonal entries: ceil(c/2) columns
+    within +-near_width of i (clipped), the rest uniform in [0, n); values
+    U(-1, 0); entries landing on the diagonal are dropped.  The pattern is
+    symmetrised by adding (i, j, v) and (j, i, v) and summing duplicates (in
+    sorted order, deterministic), then a_ii = 1.01 * sum_j |a_ij| (strictly
+    diagonally dominant -> SPD).  Returns a DeviceCsrMatrix (int32 indices).
+    """
+    import torch
+    from .sparse import DeviceCsrMatrix
+    dev = torch.device(device)
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed)
+    cnt = torch.randint(cmin, cmax + 1, (n,), generator=g, device=dev)
+    T = int(cnt.sum())
+    rows = torch.repeat_interleave(torch.arange(n, device=dev), cnt)
+    start = torch.cumsum(cnt, 0) - cnt
+    k = torch.arange(T, device=dev) - torch.repeat_interleave(start, cnt)
+    near = k < torch.repeat_interleave((cnt + 1) // 2, cnt)
+    del k, start
+    d = torch.randint(1, near_width + 1, (T,), generator=g, device=dev)
+    sgn = torch.randint(0, 2, (T,), generator=g, device=dev) * 2 - 1
+    far = torch.randint(0, n, (T,), generator=g, device=dev)
+    cols = torch.where(near, (rows + sgn * d).clamp(0, n - 1), far)
+    del d, sgn, far, near
+    vals = -torch.rand(T, generator=g, device=dev, dtype=torch.float64)
+    keep = cols != rows
+    rows, cols, vals = rows[keep], cols[keep], vals[keep]
+    del keep
+    # duplicates are summed per UNORDERED pair (canonical key min*n + max, in
+    # draw order, deterministic) and the sum is mirrored, so A is exactly
+    # symmetric
+    lo = torch.minimum(rows, cols)
+    hi = torch.maximum(rows, cols)
+    del rows, cols
+    key, order = torch.sort(lo * n + hi, stable=True)
+    del lo, hi
+    v = vals[order]
+    del vals, order
+    first = torch.ones_like(key, dtype=torch.bool)
+    first[1:] = key[1:] != key[:-1]
+    run = torch.cumsum(first, 0) - 1
+    out = v[first].clone()
+    pos = torch.arange(key.numel(), device=dev) - torch.nonzero(first).squeeze(1)[run]
+    r = 1
+    while True:  # head + 2nd + 3rd ... of each run, in draw order
+        sel = pos == r
+        if not bool(sel.any()):
+            break
+        out.index_add_(0, run[sel], v[sel])
+        r += 1
+    pkey = key[first]
+    del key, v, first, run, pos
+    pa, pb = pkey // n, pkey % n
+    del pkey
+    key2, order = torch.sort(torch.cat([pa * n + pb, pb * n + pa]))
+    out = torch.cat([out, out])[order]
+    del pa, pb, order
+    nu = key2.numel()
+    urow = key2 // n
+    ucol = key2 % n
+    del key2
+    counts = torch.bincount(urow, minlength=n)
+    rp_u = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+    rp_u[1:] = torch.cumsum(counts, 0)
+    cs = torch.zeros(nu + 1, dtype=torch.float64, device=dev)
+    cs[1:] = torch.cumsum(out.abs(), 0)
+    rowsum = cs[rp_u[1:]] - cs[rp_u[:-1]]
+    del cs
+    diag = 1.01 * rowsum
+    nnz = nu + n
+    # final index: off-diagonal entry e of row r -> e + r + [col > r]; diagonal
+    # of row r -> rp_u[r] + (#entries of row r with col < r) + r
+    e = torch.arange(nu, device=dev)
+    fidx = e + urow + (ucol > urow).to(torch.int64)
+    del e
+    col_f = torch.empty(nnz, dtype=torch.int32, device=dev)
+    val_f = torch.empty(nnz, dtype=torch.float64, device=dev)
+    col_f[fidx] = ucol.to(torch.int32)
+    val_f[fidx] = out
+    below = torch.bincount(urow[ucol < urow], minlength=n)
+    didx = rp_u[:-1] + below + torch.arange(n, device=dev)
+    col_f[didx] = torch.arange(n, device=dev, dtype=torch.int32)
+    val_f[didx] = diag
+    rp_f = (rp_u + torch.arange(n + 1, device=dev)).to(torch.int32)
+    del urow, ucol, out, fidx, didx, rp_u, below
+    torch.cuda.empty_cache() if dev.type == "cuda" else None
+    return DeviceCsrMatrix(n, n, rp_f, col_f, val_f) if dev.type == "cuda" else \
+        (rp_f, col_f, val_f)
+
+
+def config5(n=16_000_000, seed=3):
+    """C5: random irregular SPD (multi-GPU config), n = 16M, ~1.3e9 nnz, built
+    on the GPU; b ~ U(-1,1) from default_rng(seed); eps 1e-12 (DW, QTW)."""
+    A = random_irregular_spd(n, seed=seed)
+    b = np.random.default_rng(seed).uniform(-1.0, 1.0, n)
+    return dict(name="C5", A=A, b=b, x_star=None, epsilon=1e-12, max_iterations=20000)
+
+
+CONFIGS = {"C1": config1, "C2": config2, "C3": config3, "C4": config4, "C5": config5}

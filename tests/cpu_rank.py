@@ -39,6 +39,11 @@ class CpuRank:
     def part_slice(self):
         return self.rank * self.part.tmax, self.part.tmax
 
+    def segments(self, which):  # this stand-in keeps p in SoA planes
+        off, cnt = self.p_slice() if which == "p" else self.part_slice()
+        buf = self.p_full if which == "p" else self.partials
+        return [(buf[k], off, cnt) for k in range(self.w)]
+
     def _pl(self):
         return self.p_full.numpy()[:, self.lo:self.hi]
 
