@@ -96,6 +96,13 @@ class ClockSampler:
         self.index = index
         self.proc = None
         self.lines = []
+        self.k0 = 0
+
+    def mark(self):
+        """Start of the timed region: summary() uses the samples from here on
+        (the sampler is started before warm-up so nvidia-smi's own start-up
+        does not land in the timed region)."""
+        self.k0 = len(self.lines)
 
     def __enter__(self):
         try:
@@ -124,7 +131,7 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for ln in (self.lines[self.k0:] or self.lines[-1:]):
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 7:
                 continue
@@ -205,6 +212,15 @@ def run_reference(a):
 
 
 # ---------------------------------------------------------------------------
+def _free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
 def run_ours(a):
     import torch
     import torch.distributed as dist
@@ -213,6 +229,9 @@ def run_ours(a):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     if world > 1 or a.partitioned:
+        if "RANK" not in os.environ:  # plain `python bench.py --partitioned`: one rank
+            os.environ.update(RANK="0", WORLD_SIZE="1", MASTER_ADDR="127.0.0.1",
+                              MASTER_PORT=str(_free_port()))
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2510_13536_b200 import cg, kernels, _lib
     from paper_2510_13536_b200.cg import Solver, _b_norm
@@ -259,13 +278,13 @@ def run_ours(a):
 
     # ---- value: device-resident inputs ------------------------------------
     solver = Solver(A, mode)
-    for _ in range(max(3, a.warmup)):
-        device_solve(solver)
-    barrier()
-    iters, launches = 0, 0
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
+        for _ in range(max(3, a.warmup)):
+            device_solve(solver)
+        iters, launches = 0, 0
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         barrier()
+        clk.mark()
         ev0.record()
         for _ in range(a.steps):
             res, _ = device_solve(solver)
@@ -481,22 +500,41 @@ def run_partitioned(a, world, rank, local, dist, torch):
         rs.start(b_loc, bn, None, eps, max_it)
         return dist_cg_solve([rs], ex, bn, eps, max_it, check_every=32, graph=True)
 
-    for _ in range(max(1, a.warmup)):
-        solve()
-    dist.barrier()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
+        for _ in range(max(3, a.warmup)):
+            solve()
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        clk.mark()
         e0.record()
-        its = 0
+        its = launches = 0
         for _ in range(a.steps):
-            its += solve().iterations
+            r = solve()
+            its += r.iterations
+            launches += r.launches
         e1.record()
         torch.cuda.synchronize()
     dt = e0.elapsed_time(e1) * 1e-3
-    t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+    # e2e: the same solves with this rank's b copied in from pinned host
+    # memory and its solution words copied back every step
+    b_host = torch.from_numpy(np.ascontiguousarray(b[lo:hi])).pin_memory()
+    x_host = torch.empty(tuple(rs.solution().shape), dtype=torch.float64).pin_memory()
+    dist.barrier()
+    torch.cuda.synchronize()
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2.record()
+    its_e = 0
+    for _ in range(a.steps):
+        b_loc.copy_(b_host, non_blocking=True)
+        its_e += solve().iterations
+        x_host.copy_(rs.solution(), non_blocking=True)
+    e3.record()
+    torch.cuda.synchronize()
+    dte = e2.elapsed_time(e3) * 1e-3
+    t = torch.tensor([dt, dte], dtype=torch.float64, device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    dt = float(t.item())
+    dt, dte = float(t[0].item()), float(t[1].item())
     n_c2 = 128 ** 3
     value = n * its / dt / n_c2
     if rank == 0:
@@ -509,10 +547,16 @@ def run_partitioned(a, world, rank, local, dist, torch):
                                    f"{mode.upper()} to 1e-12, row-partitioned",
                        "n": n, "nnz": A.nnz, "mode": mode,
                        "iterations_per_solve": its // a.steps,
-                       "parallelism": f"row partition over {world} GPUs: NCCL all-gather of p "
-                                      "+ tile-partial all-gather, canonical reduction",
+                       "parallelism": f"row partition over {world} GPUs: p exchange = NCCL "
+                                      f"{'neighbour halo (send/recv)' if ex.mode == 'halo' else 'all-gather'}"
+                                      " + tile-partial all-gather, canonical reduction",
+                       "p_exchange": ex.mode,
                        "value_definition": "global rows x iterations / s / 128^3"},
-            "gpu_launches": None, "clocks": clk.summary(),
+            "e2e": {"value": n * its_e / dte / n_c2, "unit": "iter/s (C2-equivalent)",
+                    "h2d_bytes_per_step": 8 * (hi - lo),
+                    "d2h_bytes_per_step": 8 * int(x_host.numel()),
+                    "note": "per rank: b slice in, solution words out"},
+            "gpu_launches": launches, "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()

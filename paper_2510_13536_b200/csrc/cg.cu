@@ -17,7 +17,9 @@
 // Reference-order mode (reduction=partitions, bitwise equal to the reference
 // cg_solve(partitions=P)) replaces the fused tile-tree dots by the reference's
 // P-partition sequential dots (two extra kernels per dot).
+#include <climits>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 #include "ops.cuh"
 #include "mwcg_internal.h"
@@ -105,9 +107,28 @@ __device__ void scalar_init(CgState *st, V<Arith<M>::W> rho) {
     }
 }
 
+__device__ __forceinline__ bool halted(const CgState *st) { return st->status != RUNNING || st->pause; }
+
 __device__ __forceinline__ bool stopped(const CgState *st, cudaGraphConditionalHandle h, int use_cond) {
-    if (st->status != RUNNING) {
+    if (halted(st)) {
         if (blockIdx.x == 0 && threadIdx.x == 0) set_cond(h, use_cond, 0u);
+        return true;
+    }
+    return false;
+}
+
+// K1 starts an iteration: it also stops at the pause point k_stop (history
+// records), which an unrolled graph body reaches mid-body.
+__device__ __forceinline__ bool stopped_k1(CgState *st, cudaGraphConditionalHandle h, int use_cond) {
+    if (halted(st)) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) set_cond(h, use_cond, 0u);
+        return true;
+    }
+    if (st->k >= st->k_stop) {  // every block sees the same k, k_stop
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            st->pause = 1;  // read by the body's later kernels only
+            set_cond(h, use_cond, 0u);
+        }
         return true;
     }
     return false;
@@ -179,7 +200,7 @@ __global__ void __launch_bounds__(SpTraits<M>::THREADS, SpTraits<M>::MINB)
     __shared__ double terms[FUSED ? W * TILE : 1];
     __shared__ double smem[W * TILE_THREADS / 32];
     __shared__ int s_last;
-    if (stopped(st, h, use_cond)) return;
+    if (stopped_k1(st, h, use_cond)) return;
     const bool norm_all = st->norm_all != 0;
     const int64_t n = g.n;
     const int dir = (int)(st->k & 1);
@@ -431,7 +452,7 @@ __global__ void __launch_bounds__(TILE_THREADS)
     using Ar = Arith<M>;
     constexpr int W = Ar::W;
     __shared__ double smem[W * TILE_THREADS / 32];
-    if (phase != 0 && st->status != RUNNING) return;
+    if (phase != 0 && halted(st)) return;
     V<W> v = reduce_partials_block<M>(part, g.part_ld, g.ntiles_glob, smem);
     if (threadIdx.x == 0) {
         cudaGraphConditionalHandle h{};
@@ -448,7 +469,7 @@ __global__ void cg_dot_part(int64_t n, const double *__restrict__ x, const doubl
                             int check_status) {
     using Ar = Arith<M>;
     constexpr int W = Ar::W;
-    if (check_status && st->status != RUNNING) return;
+    if (check_status && halted(st)) return;
     int64_t pidx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (pidx >= parts) return;
     int64_t lo = (int64_t)(((__int128)n * pidx) / parts);
@@ -465,7 +486,7 @@ __global__ void cg_ref_combine(const double *__restrict__ part, int64_t parts, C
                                cudaGraphConditionalHandle h, int use_cond) {
     using Ar = Arith<M>;
     constexpr int W = Ar::W;
-    if (phase != 0 && st->status != RUNNING) {
+    if (phase != 0 && halted(st)) {
         set_cond(h, use_cond, 0u);
         return;
     }
@@ -531,6 +552,7 @@ struct mwcg_solver {
     mwcg_solver_config cfg{};
     int64_t n = 0, ntiles = 0, parts = 1;
     bool fused = true;
+    int unroll = 8;  // CG iterations per WHILE-body run (MWCG_UNROLL)
     cudaStream_t stream = nullptr;       // caller's stream (all work ordered on it)
     cudaStream_t cap = nullptr;          // private stream for graph capture
     double *x = nullptr, *r = nullptr, *p = nullptr, *q = nullptr;
@@ -698,7 +720,11 @@ int build_graph(mwcg_solver *s) {
     cudaGraph_t body = cp.conditional.phGraph_out[0];
     MWCG_CUDA(cudaStreamBeginCaptureToGraph(s->cap, body, nullptr, nullptr, 0,
                                             cudaStreamCaptureModeThreadLocal));
-    int rc = enqueue_iteration_mode(s, s->cap, s->cond, 1);
+    // U iterations per body run: one conditional evaluation per U
+    // iterations; an iteration after a stop (or the k_stop pause) launches
+    // kernels that return at once
+    int rc = 0;
+    for (int u = 0; u < s->unroll && !rc; u++) rc = enqueue_iteration_mode(s, s->cap, s->cond, 1);
     cudaGraph_t out_graph;
     cudaError_t e = cudaStreamEndCapture(s->cap, &out_graph);
     if (rc) return rc;
@@ -828,6 +854,7 @@ int mwcg_solver_create(mwcg_solver **out, const mwcg_matrix *A, const mwcg_solve
     s->n = s->A.n_rows;
     s->ntiles = num_tiles(s->n);
     s->fused = cfg->reduction != MWCG_RED_PARTITIONS;
+    if (const char *u = std::getenv("MWCG_UNROLL")) s->unroll = std::max(1, std::min(16, std::atoi(u)));
     s->parts = s->fused ? 1 : cfg->partitions;
     s->stream = (cudaStream_t)stream;
     s->geo = Geo{s->n, s->n, s->n, 0, s->ntiles, 0, s->ntiles, s->ntiles, 1};
@@ -999,7 +1026,7 @@ int mwcg_solver_start(mwcg_solver *s, const double *b, double b_norm, const doub
     init.b_norm = (b_norm == 0.0) ? 1.0 : b_norm;
     init.eps = epsilon;
     init.max_iters = max_iterations;
-    init.k_stop = 0;
+    init.k_stop = LLONG_MAX;  // no pause point until mwcg_solver_run sets one
     const bool quasi = (s->mode == QDW || s->mode == QTW);
     init.norm_r = quasi && s->cfg.normalization != MWCG_NORM_NONE;
     init.norm_all = quasi && s->cfg.normalization == MWCG_NORM_EVERY_OP;
@@ -1073,6 +1100,7 @@ int mwcg_solver_run(mwcg_solver *s, int64_t k_stop) {
     MWCG_CUDA(cudaStreamSynchronize(st));
     *s->kstop_host = (long long)k_stop;
     MWCG_CUDA(cudaMemcpyAsync(&s->st->k_stop, s->kstop_host, sizeof(long long), cudaMemcpyHostToDevice, st));
+    MWCG_CUDA(cudaMemsetAsync(&s->st->pause, 0, sizeof(int), st));
     MWCG_CUDA(cudaGraphLaunch(s->exec, st));
     return 0;
 }
@@ -1090,6 +1118,7 @@ int mwcg_solver_run_profiled(mwcg_solver *s, int64_t k_stop, double *ms) {
     MWCG_CUDA(cudaStreamSynchronize(st));
     *s->kstop_host = (long long)k_stop;
     MWCG_CUDA(cudaMemcpyAsync(&s->st->k_stop, s->kstop_host, sizeof(long long), cudaMemcpyHostToDevice, st));
+    MWCG_CUDA(cudaMemsetAsync(&s->st->pause, 0, sizeof(int), st));
     MWCG_CUDA(cudaMemcpyAsync(s->st_host, s->st, sizeof(CgState), cudaMemcpyDeviceToHost, st));
     MWCG_CUDA(cudaStreamSynchronize(st));
     cudaGraphConditionalHandle h{};
@@ -1292,7 +1321,10 @@ int mwcg_cg_solve(mwcg_solver *s, const double *b, double b_norm, const double *
         return 0;
     };
     if ((rc = record(0, stt.rel))) return rc;
+    int64_t body_kernels = 0;  // kernels launched by the iteration loop
+    const int per_it = s->fused ? 3 : 7;
     while (stt.status == RUNNING) {
+        const int64_t k_before = stt.k;
         int64_t next = (stt.k / history_stride + 1) * history_stride;
         if (next > max_iterations) next = max_iterations;
         if (profile) {
@@ -1303,6 +1335,14 @@ int mwcg_cg_solve(mwcg_solver *s, const double *b, double b_norm, const double *
             MWCG_CUDA(cudaEventRecord(s->ev[7], s->stream));
         }
         if ((rc = mwcg_solver_state(s, &stt))) return rc;
+        {
+            // iterations this run executed (a breakdown is counted as one
+            // more: exact for a K1 breakdown, which does not advance k)
+            const int64_t d = stt.k - k_before + (stt.status == BREAKDOWN ? 1 : 0);
+            // graph: whole bodies of `unroll` iterations (the tail returns at once)
+            body_kernels += profile ? per_it * d
+                                    : (int64_t)per_it * s->unroll * std::max<int64_t>(1, (d + s->unroll - 1) / s->unroll);
+        }
         if (!profile) {
             float ms = 0;
             cudaEventElapsedTime(&ms, s->ev[6], s->ev[7]);
@@ -1322,11 +1362,8 @@ int mwcg_cg_solve(mwcg_solver *s, const double *b, double b_norm, const double *
     res->n_hist = nh;
     res->loop_ms = profile ? (stage_ms[0] + stage_ms[1] + stage_ms[2]) : loop_ms;
     res->history_ms = hist_ms;
-    // kernels launched by this solve: SpMV + init, 3 per graph-body run (the
-    // body also runs once for an iteration that breaks down in K1), metrics
-    // (a breakdown is counted as one extra body run: exact for a K1 breakdown)
-    const int64_t bodies = stt.k + (stt.status == BREAKDOWN ? 1 : 0);
-    res->launches = 2 + (s->fused ? 3 : 7) * bodies + metric_launches;
+    // kernels launched by this solve: SpMV + init, the iteration loop, metrics
+    res->launches = 2 + body_kernels + metric_launches;
     res->stage_ms[0] = stage_ms[0];
     res->stage_ms[1] = stage_ms[1];
     res->stage_ms[2] = stage_ms[2];

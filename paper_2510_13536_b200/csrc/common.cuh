@@ -70,7 +70,8 @@ struct CgState {
     int status;
     int norm_r;          // normalize r (quasi & policy != none)
     int norm_all;        // every-op normalization
-    int pad0;
+    int pause;           // K1 reached k_stop inside an unrolled graph body:
+                         // the rest of the body is skipped (cleared by the host)
     unsigned int ticket[4];  // last-block-done counters
     double metrics[4];   // err^2 sum, res^2 sum (collapsed), bnorm_sq, xs_sq
 };

@@ -108,6 +108,12 @@ class RankSolver:
         self.handle = h
         import weakref
         self._fin = weakref.finalize(self, L.mwcg_solver_destroy, h)
+        self.col_range = column_range(A_local)
+
+    def p_rows(self, lo, hi):
+        """Contiguous views of the p replica for global rows [lo, hi) (AoS:
+        one block)."""
+        return [self.p_full[lo:hi]]
 
     # slices this rank contributes to the gathers
     def p_slice(self):
@@ -146,10 +152,54 @@ class RankSolver:
         return self.x[:, :self.n]
 
 
+def column_range(A):
+    """[min, max] global column referenced by A's rows ((0, -1) if none)."""
+    if A.nnz == 0:
+        return (0, -1)
+    ci = A.col_idx
+    if isinstance(ci, torch.Tensor):
+        return (int(ci.min()), int(ci.max()))
+    return (int(ci.min()), int(ci.max()))
+
+
+def halo_plan(part, ranges, max_fraction=0.5):
+    """Point-to-point pieces of p each rank needs: rank r needs the columns
+    [cmin_r, cmax_r] of p; the piece owned by rank s is the overlap with s's
+    rows.  Returns {(src, dst): (lo, hi)} row intervals, or None when the
+    halo would move more than max_fraction of an all-gather (random columns:
+    C5) -- then p is all-gathered."""
+    pieces, vol = {}, 0
+    for r, (cmin, cmax) in enumerate(ranges):
+        for sr in range(part.world):
+            if sr == r:
+                continue
+            lo_s, hi_s = part.rows(sr)
+            lo, hi = max(cmin, lo_s), min(cmax + 1, hi_s)
+            if lo < hi:
+                pieces[(sr, r)] = (lo, hi)
+                vol += hi - lo
+    full = part.world * (part.world - 1) * part.nmax
+    if full == 0 or vol > max_fraction * full:
+        return None
+    return pieces
+
+
 class LocalExchange:
     """R ranks in one process (one GPU): copy each rank's slice to the others."""
 
+    def __init__(self):
+        self.pieces = None
+
+    def setup(self, ranks):
+        self.pieces = halo_plan(ranks[0].part, [rs.col_range for rs in ranks])
+        self.mode = "halo" if self.pieces is not None else "allgather"
+
     def gather(self, ranks, which):
+        if which == "p" and self.pieces is not None:
+            for (src, dst), (lo, hi) in self.pieces.items():
+                for d, s_ in zip(ranks[dst].p_rows(lo, hi), ranks[src].p_rows(lo, hi)):
+                    d.copy_(s_)
+            return
         for src in ranks:
             for j, (buf, off, cnt) in enumerate(src.segments(which)):
                 seg = buf[off:off + cnt]
@@ -167,9 +217,39 @@ class TorchDistExchange:
         self.dist = dist
         self.group = group
         self.nccl = dist.get_backend(group) == "nccl"
+        self.pieces = None
+
+    def setup(self, ranks):
+        """All ranks exchange their column ranges once and derive the same
+        halo plan (or fall back to the all-gather)."""
+        (me,) = ranks
+        world = self.dist.get_world_size(self.group)
+        dev = me.p_full.device
+        t = torch.tensor(list(me.col_range), dtype=torch.int64, device=dev)
+        allr = [torch.empty_like(t) for _ in range(world)]
+        self.dist.all_gather(allr, t, group=self.group)
+        ranges = [tuple(int(v) for v in a.cpu()) for a in allr]
+        self.pieces = halo_plan(me.part, ranges)
+        self.mode = "halo" if self.pieces is not None else "allgather"
+
+    def _halo(self, me):
+        ops = []
+        for (src, dst), (lo, hi) in sorted(self.pieces.items()):
+            if src == me.rank:
+                ops += [self.dist.P2POp(self.dist.isend, seg, dst, group=self.group)
+                        for seg in me.p_rows(lo, hi)]
+            elif dst == me.rank:
+                ops += [self.dist.P2POp(self.dist.irecv, seg, src, group=self.group)
+                        for seg in me.p_rows(lo, hi)]
+        if ops:
+            for req in self.dist.batch_isend_irecv(ops):
+                req.wait()
 
     def gather(self, ranks, which):
         (me,) = ranks
+        if which == "p" and self.pieces is not None:
+            self._halo(me)
+            return
         for buf, off, cnt in me.segments(which):
             if self.nccl:  # in-place: each rank's slice already sits at off = rank*cnt
                 self.dist.all_gather_into_tensor(buf, buf[off:off + cnt], group=self.group)
@@ -187,6 +267,10 @@ class DistResult:
     reason: str
     iterations: int
     final_recurrence_residual: float
+    launches: int = 0  # kernels one rank launched (start + stages; graph replays counted)
+
+
+STAGES_PER_ITERATION = 5
 
 
 def _iteration(ranks, exchange):
@@ -215,16 +299,30 @@ def dist_cg_solve(ranks, exchange, b_norm, epsilon=1e-12, max_iterations=None,
     stop test early-exit on the device status; the segment's remaining
     exchanges are harmless."""
     part = ranks[0].part
+    if getattr(exchange, "setup", None) is not None and getattr(exchange, "_ready", None) is not ranks[0]:
+        exchange.setup(ranks)
+        exchange._ready = ranks[0]
     exchange.gather(ranks, "part")
     for rs in ranks:
         rs.stage("final_init")
     exchange.gather(ranks, "p")
     st = ranks[0].state()
-    g = None
-    if graph and st.status == 0:
-        # one eager segment first (NCCL communicators / lazy init), then capture
+    calls = 0
+    cache = getattr(ranks[0], "_graphs", None)
+    if cache is None:
+        cache = {}
+        try:
+            ranks[0]._graphs = cache
+        except AttributeError:  # pragma: no cover
+            pass
+    key = (id(exchange), check_every)
+    g = cache.get(key) if graph else None
+    if graph and g is None and st.status == 0:
+        # one eager segment first (NCCL communicators / lazy init), then
+        # capture; the graph is kept on the rank (same buffers every solve)
         for _ in range(check_every):
             _iteration(ranks, exchange)
+        calls += check_every
         st = ranks[0].state()
         if st.status == 0:
             try:
@@ -233,6 +331,8 @@ def dist_cg_solve(ranks, exchange, b_norm, epsilon=1e-12, max_iterations=None,
                     for _ in range(check_every):
                         _iteration(ranks, exchange)
                 g.replay()   # the captured segment is not executed by capture itself
+                cache[key] = g
+                calls += check_every
             except Exception:  # pragma: no cover - capture unsupported: stay eager
                 g = None
                 torch.cuda.synchronize()
@@ -243,9 +343,12 @@ def dist_cg_solve(ranks, exchange, b_norm, epsilon=1e-12, max_iterations=None,
         else:
             for _ in range(check_every):
                 _iteration(ranks, exchange)
+        calls += check_every
         st = ranks[0].state()
     reason = _lib.STATUS[st.status]
-    return DistResult(reason == "converged", reason, int(st.iterations), float(st.rel))
+    # start: x0 spread + SpMV + init stage; final_init; 5 stage kernels per iteration
+    launches = 3 + 1 + STAGES_PER_ITERATION * calls
+    return DistResult(reason == "converged", reason, int(st.iterations), float(st.rel), launches)
 
 
 def solve_partitioned(A, b, world, mode="dw", epsilon=1e-12, max_iterations=None, x0=None,

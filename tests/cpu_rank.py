@@ -32,12 +32,17 @@ class CpuRank:
         self.norm_all = quasi and normalization == "every-op"
         self.tile_off = part.tiles(rank)[0]
         self.st = SimpleNamespace(status=0, k=0, iterations=0, rel=0.0)
+        ci = A_local.col_idx
+        self.col_range = (int(ci.min()), int(ci.max())) if ci.size else (0, -1)
 
     def p_slice(self):
         return self.rank * self.part.nmax, self.part.nmax
 
     def part_slice(self):
         return self.rank * self.part.tmax, self.part.tmax
+
+    def p_rows(self, lo, hi):  # SoA planes: one contiguous view per word
+        return [self.p_full[j, lo:hi] for j in range(self.w)]
 
     def segments(self, which):  # this stand-in keeps p in SoA planes
         off, cnt = self.p_slice() if which == "p" else self.part_slice()

@@ -67,3 +67,37 @@ def test_partitioned_graph_replay_equals_eager(mode):
     res, x = solve_partitioned(A, b, 3, mode=mode, epsilon=1e-20, check_every=8, graph=True)
     assert res.iterations == single.iterations
     assert np.array_equal(_bits(x), _bits(single.x.planes))
+
+
+@pytest.mark.parametrize("mode", ["dw", "tw"])
+def test_partitioned_cached_graph_second_solve(mode):
+    """A second solve on the same ranks replays the cached segment graph (no
+    eager segment, no re-capture) and reproduces the first solve bitwise;
+    the banded matrix takes the neighbour-halo exchange."""
+    from paper_2510_13536_b200.cg import _b_norm
+    from paper_2510_13536_b200.dist import (LocalExchange, RankSolver, dist_cg_solve, local_rows,
+                                            partition)
+    A = laplacian_2d(100)
+    xs = np.random.default_rng(5).uniform(-1, 1, A.n_rows)
+    b = problems.spmv_fp64_host(A, xs)
+    part = partition(A.n_rows, 3)
+    ranks, bl = [], []
+    for r in range(3):
+        lo, hi = part.rows(r)
+        ranks.append(RankSolver(local_rows(A, lo, hi), part, r, mode))
+        bl.append(torch.from_numpy(np.ascontiguousarray(b[lo:hi])).cuda())
+    ex = LocalExchange()
+    out = []
+    for _ in range(2):
+        for rs, bb in zip(ranks, bl):
+            rs.start(bb, _b_norm(b), None, 1e-20, 10 * A.n_rows)
+        res = dist_cg_solve(ranks, ex, _b_norm(b), 1e-20, None, check_every=8, graph=True)
+        out.append((res, torch.cat([rs.solution() for rs in ranks], dim=1).clone()))
+    assert ex.mode == "halo"
+    assert len(ranks[0]._graphs) == 1
+    (r1, x1), (r2, x2) = out
+    assert r1.iterations == r2.iterations and r1.launches == r2.launches
+    assert np.array_equal(_bits(x1), _bits(x2))
+    single = cg.cg_solve(A, b, cg.SolverConfig(mode=mode, epsilon=1e-20, history_stride=10**6))
+    assert r1.iterations == single.iterations
+    assert np.array_equal(_bits(x1), _bits(single.x.planes))

@@ -48,9 +48,28 @@ def launches(path):
     return [{"id": k[0], "kernel": k[1], **v} for k, v in sorted(data.items())]
 
 
+def launches_agg(path, command, note):
+    """Launch list plus a per-kernel aggregate (count, mean/total time, share)."""
+    ls = launches(path)
+    agg = {}
+    for e in ls:
+        t = float(e["gpu__time_duration.sum"].split()[0].replace(",", ""))
+        a = agg.setdefault(e["kernel"].split("(")[0], {"launches": 0, "total_ns": 0.0})
+        a["launches"] += 1
+        a["total_ns"] += t
+    tot = sum(a["total_ns"] for a in agg.values())
+    for a in agg.values():
+        a["mean_ns"] = a["total_ns"] / a["launches"]
+        a["share"] = a["total_ns"] / tot
+    return {"command": command, "note": note, "per_kernel": agg, "launches": ls}
+
+
 if __name__ == "__main__":
     kind, src, dst = sys.argv[1:4]
-    obj = report(src) if kind == "report" else launches(src)
+    if kind == "launches-agg":
+        obj = launches_agg(src, sys.argv[4], sys.argv[5] if len(sys.argv) > 5 else "")
+    else:
+        obj = report(src) if kind == "report" else launches(src)
     with open(dst, "w") as f:
         json.dump(obj, f, indent=1)
     print("wrote", dst, len(obj))
