@@ -22,6 +22,7 @@
 #include <cstdlib>
 #include <vector>
 #include "ops.cuh"
+#include "tma.cuh"
 #include "mwcg_internal.h"
 #include "../../include/mwcg_cuda.h"
 
@@ -377,6 +378,226 @@ __global__ void __launch_bounds__(TILE_THREADS)
     }
 }
 
+// ---------------------------------------------------------------- TMA-staged K2 / K3
+// The vector passes are pure streams: each tile's operands (x, r, q word
+// planes, the AoS slice of p) are contiguous 8-KB runs, so one thread issues
+// them as 1-D bulk copies (cp.async.bulk) into a shared-memory ring of NS
+// stages and the copy engine, not registers, holds the bytes in flight.
+// One CTA of TILE_THREADS threads per SM; the canonical tile mapping
+// (thread t: elements t + j*256) and the canonical r.r tree are unchanged,
+// so results are bitwise those of cg_update / cg_xpay.  A partial last tile
+// is read with plain loads (its stage is completed by a plain arrive, so the
+// ring's phase bits stay in step).  Requires 16-B aligned planes (ld even).
+template <int M>
+struct UpTma {
+    static constexpr int W = Arith<M>::W;
+    static constexpr int STAGE = 4 * W * TILE;  // doubles: x, r, q planes + p AoS
+    static constexpr int NS = (M == FP64) ? 4 : (W == 2 ? 3 : 2);
+    static constexpr size_t SMEM = sizeof(double) * STAGE * NS;
+};
+template <int M>
+struct XpTma {
+    static constexpr int W = Arith<M>::W;
+    static constexpr int STAGE = 2 * W * TILE;  // r planes + p AoS
+    static constexpr int NS = (M == FP64) ? 6 : (W == 2 ? 5 : 4);
+    static constexpr size_t SMEM = sizeof(double) * STAGE * NS;
+};
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <int M>
+__device__ __forceinline__ void up_issue(double *stage, uint64_t *bar, const double *x, const double *r,
+                                         const double *q, const double *pl, int64_t ld, int64_t tile,
+                                         bool full) {
+    constexpr int W = Arith<M>::W;
+    if (!full) {
+        mbar_arrive(bar);
+        return;
+    }
+    constexpr uint32_t PB = TILE * sizeof(double);
+    mbar_arrive_expect_tx(bar, 4u * W * PB);
+    const int64_t e0 = tile * TILE;
+#pragma unroll
+    for (int k = 0; k < W; k++) {
+        bulk_g2s(stage + (0 * W + k) * TILE, x + k * ld + e0, PB, bar);
+        bulk_g2s(stage + (1 * W + k) * TILE, r + k * ld + e0, PB, bar);
+        bulk_g2s(stage + (2 * W + k) * TILE, q + k * ld + e0, PB, bar);
+    }
+    bulk_g2s(stage + 3 * W * TILE, pl + e0 * W, W * PB, bar);
+}
+
+template <int M, bool FUSED>
+__global__ void __launch_bounds__(TILE_THREADS, 1)
+    cg_update_tma(double *__restrict__ x, double *__restrict__ r, const double *__restrict__ p,
+                  const double *__restrict__ q, Geo g, double *__restrict__ part, CgState *st,
+                  cudaGraphConditionalHandle h, int use_cond) {
+    using Ar = Arith<M>;
+    using T = UpTma<M>;
+    constexpr int W = Ar::W;
+    extern __shared__ __align__(128) double ring[];
+    __shared__ uint64_t bar[T::NS];
+    __shared__ double smem[W * TILE_THREADS / 32];
+    __shared__ int s_last;
+    if (stopped(st, h, use_cond)) return;
+    const bool norm_all = st->norm_all != 0, norm_r = st->norm_r != 0;
+    V<W> alpha, nalpha;
+#pragma unroll
+    for (int k = 0; k < W; k++) {
+        alpha.w[k] = st->alpha[k];
+        nalpha.w[k] = st->neg_alpha[k];
+    }
+    const int64_t n = g.n, ld = g.ld;
+    const double *__restrict__ pl = p + g.p_off * W;
+    const int dir = (int)((st->k & 1) ^ 1);
+    const int64_t nmine = g.ntiles > blockIdx.x ? (g.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < T::NS; i++) mbar_init(&bar[i], 1);
+        mbar_init_fence();
+        for (int64_t i = 0; i < T::NS && i < nmine; i++) {
+            const int64_t tile = snake(blockIdx.x + i * gridDim.x, g.ntiles, dir);
+            up_issue<M>(ring + i * T::STAGE, &bar[i], x, r, q, pl, ld, tile, (tile + 1) * TILE <= n);
+        }
+    }
+    __syncthreads();
+    for (int64_t i = 0; i < nmine; i++) {
+        const int64_t tile = snake(blockIdx.x + i * gridDim.x, g.ntiles, dir);
+        const int sidx = (int)(i % T::NS);
+        const double *sg = ring + sidx * T::STAGE;
+        const bool full = (tile + 1) * TILE <= n;
+        mbar_wait(&bar[sidx], (uint32_t)((i / T::NS) & 1));
+        const int64_t base = tile * TILE + threadIdx.x;
+        V<W> acc = zero<W>();
+#pragma unroll
+        for (int j = 0; j < TILE_ELEMS; j++) {
+            const int li = threadIdx.x + j * TILE_THREADS;
+            const int64_t e = base + j * TILE_THREADS;
+            V<W> xv, pv, rv, qv;
+            if (full) {
+#pragma unroll
+                for (int k = 0; k < W; k++) {
+                    xv.w[k] = sg[(0 * W + k) * TILE + li];
+                    rv.w[k] = sg[(1 * W + k) * TILE + li];
+                    qv.w[k] = sg[(2 * W + k) * TILE + li];
+                    pv.w[k] = sg[3 * W * TILE + li * W + k];
+                }
+            } else if (e < n) {
+                xv = load<W>(x, ld, e);
+                pv = load_aos_ro<W>(pl, e);
+                rv = load<W>(r, ld, e);
+                qv = load_ro<W>(q, ld, e);
+            }
+            if (e < n) {
+                V<W> xi = Ar::add(xv, Ar::mul(alpha, pv));
+                if (norm_all) xi = Ar::norm(xi);
+                store<W>(x, ld, e, xi);
+                V<W> ri = Ar::add(rv, Ar::mul(nalpha, qv));
+                if (norm_r) ri = Ar::norm(ri);
+                store<W>(r, ld, e, ri);
+                if (FUSED) acc = Ar::add(acc, Ar::mul(ri, ri));
+            }
+        }
+        __syncthreads();  // every thread is done reading stage sidx
+        if (threadIdx.x == 0 && i + T::NS < nmine) {
+            fence_proxy_async_smem();
+            const int64_t nt = snake(blockIdx.x + (i + T::NS) * gridDim.x, g.ntiles, dir);
+            up_issue<M>(ring + sidx * T::STAGE, &bar[sidx], x, r, q, pl, ld, nt, (nt + 1) * TILE <= n);
+        }
+        if (FUSED) {
+            acc = block_tree<M, TILE_THREADS>(acc, smem);
+            if (threadIdx.x == 0) store<W>(part, g.part_ld, g.tile_off + tile, acc);
+        }
+    }
+    if (!FUSED || !g.final_) return;
+    if (!last_block_done(&st->ticket[1], &s_last)) return;
+    V<W> rn = reduce_partials_block<M>(part, g.part_ld, g.ntiles_glob, smem);
+    if (threadIdx.x == 0) {
+        st->ticket[1] = 0u;
+        scalar_beta<M>(st, rn, h, use_cond);
+    }
+}
+
+template <int M>
+__device__ __forceinline__ void xp_issue(double *stage, uint64_t *bar, const double *r, const double *pl,
+                                         int64_t ld, int64_t tile, bool full) {
+    constexpr int W = Arith<M>::W;
+    if (!full) {
+        mbar_arrive(bar);
+        return;
+    }
+    constexpr uint32_t PB = TILE * sizeof(double);
+    mbar_arrive_expect_tx(bar, 2u * W * PB);
+    const int64_t e0 = tile * TILE;
+#pragma unroll
+    for (int k = 0; k < W; k++) bulk_g2s(stage + k * TILE, r + k * ld + e0, PB, bar);
+    bulk_g2s(stage + W * TILE, pl + e0 * W, W * PB, bar);
+}
+
+template <int M>
+__global__ void __launch_bounds__(TILE_THREADS, 1)
+    cg_xpay_tma(double *__restrict__ p, const double *__restrict__ r, Geo g, CgState *st,
+                cudaGraphConditionalHandle h, int use_cond) {
+    using Ar = Arith<M>;
+    using T = XpTma<M>;
+    constexpr int W = Ar::W;
+    extern __shared__ __align__(128) double ring[];
+    __shared__ uint64_t bar[T::NS];
+    if (stopped(st, h, use_cond)) return;
+    const bool norm_all = st->norm_all != 0;
+    V<W> beta;
+#pragma unroll
+    for (int k = 0; k < W; k++) beta.w[k] = st->beta[k];
+    const int64_t n = g.n, ld = g.ld;
+    double *__restrict__ pl = p + g.p_off * W;
+    const int dir = (int)((st->k & 1) ^ 1);
+    const int64_t nmine = g.ntiles > blockIdx.x ? (g.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < T::NS; i++) mbar_init(&bar[i], 1);
+        mbar_init_fence();
+        for (int64_t i = 0; i < T::NS && i < nmine; i++) {
+            const int64_t tile = snake(blockIdx.x + i * gridDim.x, g.ntiles, dir);
+            xp_issue<M>(ring + i * T::STAGE, &bar[i], r, pl, ld, tile, (tile + 1) * TILE <= n);
+        }
+    }
+    __syncthreads();
+    for (int64_t i = 0; i < nmine; i++) {
+        const int64_t tile = snake(blockIdx.x + i * gridDim.x, g.ntiles, dir);
+        const int sidx = (int)(i % T::NS);
+        const double *sg = ring + sidx * T::STAGE;
+        const bool full = (tile + 1) * TILE <= n;
+        mbar_wait(&bar[sidx], (uint32_t)((i / T::NS) & 1));
+        const int64_t base = tile * TILE + threadIdx.x;
+#pragma unroll
+        for (int j = 0; j < TILE_ELEMS; j++) {
+            const int li = threadIdx.x + j * TILE_THREADS;
+            const int64_t e = base + j * TILE_THREADS;
+            V<W> rv, pv;
+            if (full) {
+#pragma unroll
+                for (int k = 0; k < W; k++) {
+                    rv.w[k] = sg[k * TILE + li];
+                    pv.w[k] = sg[W * TILE + li * W + k];
+                }
+            } else if (e < n) {
+                rv = load_ro<W>(r, ld, e);
+                pv = load_aos<W>(pl, e);
+            }
+            if (e < n) {
+                V<W> pi = Ar::add(rv, Ar::mul(beta, pv));
+                if (norm_all) pi = Ar::norm(pi);
+                store_aos<W>(pl, e, pi);
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && i + T::NS < nmine) {
+            fence_proxy_async_smem();
+            const int64_t nt = snake(blockIdx.x + (i + T::NS) * gridDim.x, g.ntiles, dir);
+            xp_issue<M>(ring + sidx * T::STAGE, &bar[sidx], r, pl, ld, nt, (nt + 1) * TILE <= n);
+        }
+    }
+}
+
 // ---------------------------------------------------------------- init
 // r = b - q (residual, cg.py:114), [norm r] (cg.py:115-116), p = r (117),
 // rho = r.r (118), rel, converged-at-0 test (147-148).
@@ -575,51 +796,86 @@ struct mwcg_solver {
     unsigned grid[4] = {1, 1, 1, 1};  // spmv_pq, update, xpay, init
     Geo geo{};
     bool dist = false;                   // rank of a row partition (no graph; see dist.py)
+    bool tma = false;                    // TMA-staged K2/K3 (aligned planes; MWCG_TMA=0 disables)
 };
 
 namespace {
 
-template <int M>
-int enqueue_iteration(mwcg_solver *s, cudaStream_t st, cudaGraphConditionalHandle h, int use_cond) {
-    const unsigned g0 = s->grid[0], g1 = s->grid[1], g2 = s->grid[2];
+// Stage launchers shared by the graph body, the profiled (kernel-by-kernel)
+// loop and the multi-rank driver.  fused: tile-tree dots inside K1/K2;
+// otherwise the reference-order dots (cg_dot_part + cg_ref_combine).
+template <int M, bool FUSED>
+void launch_k1(mwcg_solver *s, cudaStream_t st, cudaGraphConditionalHandle h, int use_cond) {
     const Geo &g = s->geo;
-    if (s->fused) {
-        if (s->A.col16)
-            cg_spmv_pq<M, true, int16_t><<<g0, SpTraits<M>::THREADS, 0, st>>>(s->A, s->p, s->q, g, s->part,
-                                                                              s->st, h, use_cond);
-        else
-            cg_spmv_pq<M, true, int32_t><<<g0, SpTraits<M>::THREADS, 0, st>>>(s->A, s->p, s->q, g, s->part,
-                                                                              s->st, h, use_cond);
-        cg_update<M, true><<<g1, TILE_THREADS, 0, st>>>(s->x, s->r, s->p, s->q, g, s->part, s->st, h,
-                                                         use_cond);
+    const unsigned g0 = s->grid[0];
+    if (s->A.col16)
+        cg_spmv_pq<M, FUSED, int16_t><<<g0, SpTraits<M>::THREADS, 0, st>>>(s->A, s->p, s->q, g, s->part, s->st,
+                                                                           h, use_cond);
+    else
+        cg_spmv_pq<M, FUSED, int32_t><<<g0, SpTraits<M>::THREADS, 0, st>>>(s->A, s->p, s->q, g, s->part, s->st,
+                                                                           h, use_cond);
+}
+
+template <int M, bool FUSED>
+void launch_k2(mwcg_solver *s, cudaStream_t st, cudaGraphConditionalHandle h, int use_cond) {
+    const Geo &g = s->geo;
+    if (s->tma)
+        cg_update_tma<M, FUSED><<<s->grid[1], TILE_THREADS, UpTma<M>::SMEM, st>>>(s->x, s->r, s->p, s->q, g,
+                                                                                  s->part, s->st, h, use_cond);
+    else
+        cg_update<M, FUSED><<<s->grid[1], TILE_THREADS, 0, st>>>(s->x, s->r, s->p, s->q, g, s->part, s->st, h,
+                                                                 use_cond);
+}
+
+template <int M>
+void launch_k3(mwcg_solver *s, cudaStream_t st, cudaGraphConditionalHandle h, int use_cond) {
+    if (s->tma)
+        cg_xpay_tma<M><<<s->grid[2], TILE_THREADS, XpTma<M>::SMEM, st>>>(s->p, s->r, s->geo, s->st, h, use_cond);
+    else
+        cg_xpay<M><<<s->grid[2], TILE_THREADS, 0, st>>>(s->p, s->r, s->geo, s->st, h, use_cond);
+}
+
+// stage 0: K1 [+ reference p.q], 1: K2 [+ reference r.r], 2: K3
+template <int M>
+int enqueue_stage(mwcg_solver *s, int stage, cudaStream_t st, cudaGraphConditionalHandle h, int use_cond) {
+    const unsigned pb = (unsigned)((s->parts + 127) / 128);
+    if (stage == 0) {
+        if (s->fused) {
+            launch_k1<M, true>(s, st, h, use_cond);
+        } else {
+            launch_k1<M, false>(s, st, h, use_cond);
+            cg_dot_part<M, true><<<pb, 128, 0, st>>>(s->n, s->p, s->q, s->n, s->parts, s->part, s->st, 1);
+            cg_ref_combine<M><<<1, 1, 0, st>>>(s->part, s->parts, s->st, 1, h, use_cond);
+        }
+    } else if (stage == 1) {
+        if (s->fused) {
+            launch_k2<M, true>(s, st, h, use_cond);
+        } else {
+            launch_k2<M, false>(s, st, h, use_cond);
+            cg_dot_part<M, false><<<pb, 128, 0, st>>>(s->n, s->r, s->r, s->n, s->parts, s->part, s->st, 1);
+            cg_ref_combine<M><<<1, 1, 0, st>>>(s->part, s->parts, s->st, 2, h, use_cond);
+        }
     } else {
-        const unsigned pb = (unsigned)((s->parts + 127) / 128);
-        if (s->A.col16)
-            cg_spmv_pq<M, false, int16_t><<<g0, SpTraits<M>::THREADS, 0, st>>>(s->A, s->p, s->q, g, s->part,
-                                                                               s->st, h, use_cond);
-        else
-            cg_spmv_pq<M, false, int32_t><<<g0, SpTraits<M>::THREADS, 0, st>>>(s->A, s->p, s->q, g, s->part,
-                                                                               s->st, h, use_cond);
-        cg_dot_part<M, true><<<pb, 128, 0, st>>>(s->n, s->p, s->q, s->n, s->parts, s->part, s->st, 1);
-        cg_ref_combine<M><<<1, 1, 0, st>>>(s->part, s->parts, s->st, 1, h, use_cond);
-        cg_update<M, false><<<g1, TILE_THREADS, 0, st>>>(s->x, s->r, s->p, s->q, g, s->part, s->st, h,
-                                                          use_cond);
-        cg_dot_part<M, false><<<pb, 128, 0, st>>>(s->n, s->r, s->r, s->n, s->parts, s->part, s->st, 1);
-        cg_ref_combine<M><<<1, 1, 0, st>>>(s->part, s->parts, s->st, 2, h, use_cond);
+        launch_k3<M>(s, st, h, use_cond);
     }
-    cg_xpay<M><<<g2, TILE_THREADS, 0, st>>>(s->p, s->r, g, s->st, h, use_cond);
     MWCG_CHECK_LAUNCH();
     return 0;
 }
 
-int enqueue_iteration_mode(mwcg_solver *s, cudaStream_t st, cudaGraphConditionalHandle h, int use_cond) {
+int enqueue_stage_mode(mwcg_solver *s, int stage, cudaStream_t st, cudaGraphConditionalHandle h, int use_cond) {
     switch (s->mode) {
-    case FP64: return enqueue_iteration<FP64>(s, st, h, use_cond);
-    case DW: return enqueue_iteration<DW>(s, st, h, use_cond);
-    case QDW: return enqueue_iteration<QDW>(s, st, h, use_cond);
-    case TW: return enqueue_iteration<TW>(s, st, h, use_cond);
-    default: return enqueue_iteration<QTW>(s, st, h, use_cond);
+    case FP64: return enqueue_stage<FP64>(s, stage, st, h, use_cond);
+    case DW: return enqueue_stage<DW>(s, stage, st, h, use_cond);
+    case QDW: return enqueue_stage<QDW>(s, stage, st, h, use_cond);
+    case TW: return enqueue_stage<TW>(s, stage, st, h, use_cond);
+    default: return enqueue_stage<QTW>(s, stage, st, h, use_cond);
     }
+}
+
+int enqueue_iteration_mode(mwcg_solver *s, cudaStream_t st, cudaGraphConditionalHandle h, int use_cond) {
+    for (int k = 0; k < 3; k++)
+        if (int rc = enqueue_stage_mode(s, k, st, h, use_cond)) return rc;
+    return 0;
 }
 
 template <int M>
@@ -650,21 +906,11 @@ int enqueue_dist_stage(mwcg_solver *s, int stage) {
         cg_init<M, true><<<s->grid[3], TILE_THREADS, 0, st>>>(s->b, s->q, s->r, s->p, g, s->part, s->st);
         break;
     case MWCG_STAGE_FINAL_INIT: cg_finalize<M><<<1, TILE_THREADS, 0, st>>>(s->part, g, s->st, 0); break;
-    case MWCG_STAGE_SPMV:
-        if (s->A.col16)
-            cg_spmv_pq<M, true, int16_t><<<s->grid[0], SpTraits<M>::THREADS, 0, st>>>(s->A, s->p, s->q, g,
-                                                                                      s->part, s->st, h, 0);
-        else
-            cg_spmv_pq<M, true, int32_t><<<s->grid[0], SpTraits<M>::THREADS, 0, st>>>(s->A, s->p, s->q, g,
-                                                                                      s->part, s->st, h, 0);
-        break;
+    case MWCG_STAGE_SPMV: launch_k1<M, true>(s, st, h, 0); break;
     case MWCG_STAGE_FINAL_ALPHA: cg_finalize<M><<<1, TILE_THREADS, 0, st>>>(s->part, g, s->st, 1); break;
-    case MWCG_STAGE_UPDATE:
-        cg_update<M, true><<<s->grid[1], TILE_THREADS, 0, st>>>(s->x, s->r, s->p, s->q, g, s->part, s->st, h,
-                                                                 0);
-        break;
+    case MWCG_STAGE_UPDATE: launch_k2<M, true>(s, st, h, 0); break;
     case MWCG_STAGE_FINAL_BETA: cg_finalize<M><<<1, TILE_THREADS, 0, st>>>(s->part, g, s->st, 2); break;
-    case MWCG_STAGE_XPAY: cg_xpay<M><<<s->grid[2], TILE_THREADS, 0, st>>>(s->p, s->r, g, s->st, h, 0); break;
+    case MWCG_STAGE_XPAY: launch_k3<M>(s, st, h, 0); break;
     default: set_error("unknown stage %d", stage); return MWCG_ERR_VALUE;
     }
     MWCG_CHECK_LAUNCH();
@@ -677,6 +923,13 @@ int compute_grids_t(mwcg_solver *s) {
     MWCG_CUDA(cudaGetDevice(&dev));
     MWCG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     int nb[4] = {1, 1, 1, 1};
+    {
+        // TMA-staged vector passes: measured faster for QTW (C2: K2 62.6 ->
+        // 58.1 us, K3 28.5 -> 26.6 us), neutral for DW/QDW, slower for FP64
+        // and TW; MWCG_TMA=0/1 overrides
+        const char *t = std::getenv("MWCG_TMA");
+        s->tma = t ? t[0] != '0' : (M == QTW);
+    }
     if (s->fused) {
         MWCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb[0], cg_spmv_pq<M, true, int32_t>,
                                                                 SpTraits<M>::THREADS, 0));
@@ -689,6 +942,25 @@ int compute_grids_t(mwcg_solver *s) {
         MWCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb[3], cg_init<M, false>, TILE_THREADS, 0));
     }
     MWCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb[2], cg_xpay<M>, TILE_THREADS, 0));
+    if (s->tma) {
+        // alignment of every plane the bulk copies touch (16 B)
+        const int W = Arith<M>::W;
+        auto al = [](const void *ptr) { return ((uintptr_t)ptr & 15u) == 0; };
+        s->tma = al(s->x) && al(s->r) && al(s->q) && al(s->p) && (s->geo.ld % 2 == 0) &&
+                 ((s->geo.p_off * W) % 2 == 0);
+    }
+    if (s->tma) {
+        MWCG_CUDA(cudaFuncSetAttribute(cg_update_tma<M, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)UpTma<M>::SMEM));
+        MWCG_CUDA(cudaFuncSetAttribute(cg_update_tma<M, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)UpTma<M>::SMEM));
+        MWCG_CUDA(cudaFuncSetAttribute(cg_xpay_tma<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)XpTma<M>::SMEM));
+        MWCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb[1], cg_update_tma<M, true>, TILE_THREADS,
+                                                                UpTma<M>::SMEM));
+        MWCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb[2], cg_xpay_tma<M>, TILE_THREADS,
+                                                                XpTma<M>::SMEM));
+    }
     for (int i = 0; i < 4; i++) {
         int64_t g = (int64_t)(nb[i] > 0 ? nb[i] : 1) * sms;
         if (g > s->geo.ntiles) g = s->geo.ntiles;
@@ -1124,48 +1396,10 @@ int mwcg_solver_run_profiled(mwcg_solver *s, int64_t k_stop, double *ms) {
     cudaGraphConditionalHandle h{};
     while (s->st_host->status == RUNNING && s->st_host->k < k_stop) {
         MWCG_CUDA(cudaEventRecord(s->ev[0], st));
-#define STAGES(Mx)                                                                                         \
-    do {                                                                                                   \
-        const unsigned pb = (unsigned)((s->parts + 127) / 128);                                            \
-        const Geo &g = s->geo;                                                                             \
-        if (s->fused) {                                                                                    \
-            if (s->A.col16)                                                                                \
-                cg_spmv_pq<Mx, true, int16_t><<<s->grid[0], SpTraits<Mx>::THREADS, 0, st>>>(               \
-                    s->A, s->p, s->q, g, s->part, s->st, h, 0);                                            \
-            else                                                                                           \
-                cg_spmv_pq<Mx, true, int32_t><<<s->grid[0], SpTraits<Mx>::THREADS, 0, st>>>(               \
-                    s->A, s->p, s->q, g, s->part, s->st, h, 0);                                            \
-        } else {                                                                                           \
-            if (s->A.col16)                                                                                \
-                cg_spmv_pq<Mx, false, int16_t><<<s->grid[0], SpTraits<Mx>::THREADS, 0, st>>>(              \
-                    s->A, s->p, s->q, g, s->part, s->st, h, 0);                                            \
-            else                                                                                           \
-                cg_spmv_pq<Mx, false, int32_t><<<s->grid[0], SpTraits<Mx>::THREADS, 0, st>>>(              \
-                    s->A, s->p, s->q, g, s->part, s->st, h, 0);                                            \
-            cg_dot_part<Mx, true><<<pb, 128, 0, st>>>(s->n, s->p, s->q, s->n, s->parts, s->part, s->st, 1);      \
-            cg_ref_combine<Mx><<<1, 1, 0, st>>>(s->part, s->parts, s->st, 1, h, 0);                        \
-        }                                                                                                  \
-        cudaEventRecord(s->ev[1], st);                                                                     \
-        if (s->fused) {                                                                                    \
-            cg_update<Mx, true><<<s->grid[1], TILE_THREADS, 0, st>>>(s->x, s->r, s->p, s->q, g, s->part,   \
-                                                                      s->st, h, 0);                        \
-        } else {                                                                                           \
-            cg_update<Mx, false><<<s->grid[1], TILE_THREADS, 0, st>>>(s->x, s->r, s->p, s->q, g, s->part,  \
-                                                                       s->st, h, 0);                       \
-            cg_dot_part<Mx, false><<<pb, 128, 0, st>>>(s->n, s->r, s->r, s->n, s->parts, s->part, s->st, 1);      \
-            cg_ref_combine<Mx><<<1, 1, 0, st>>>(s->part, s->parts, s->st, 2, h, 0);                        \
-        }                                                                                                  \
-        cudaEventRecord(s->ev[2], st);                                                                     \
-        cg_xpay<Mx><<<s->grid[2], TILE_THREADS, 0, st>>>(s->p, s->r, g, s->st, h, 0);                     \
-    } while (0)
-        switch (s->mode) {
-        case FP64: STAGES(FP64); break;
-        case DW: STAGES(DW); break;
-        case QDW: STAGES(QDW); break;
-        case TW: STAGES(TW); break;
-        default: STAGES(QTW); break;
+        for (int k = 0; k < 3; k++) {
+            if (int rc = enqueue_stage_mode(s, k, st, h, 0)) return rc;
+            if (k < 2) MWCG_CUDA(cudaEventRecord(s->ev[1 + k], st));
         }
-#undef STAGES
         MWCG_CHECK_LAUNCH();
         MWCG_CUDA(cudaEventRecord(s->ev[3], st));
         MWCG_CUDA(cudaMemcpyAsync(s->st_host, s->st, sizeof(CgState), cudaMemcpyDeviceToHost, st));

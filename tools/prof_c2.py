@@ -11,6 +11,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--modes", default="dw")
 ap.add_argument("--iters", type=int, default=3)
 ap.add_argument("--peak", action="store_true")
+ap.add_argument("--red", default="tile")
 a = ap.parse_args()
 if a.peak:
     L = _lib.load()
@@ -21,5 +22,6 @@ if a.peak:
 c = problems.config2()
 for mode in a.modes.split(","):
     r = cg.cg_solve(c["A"], c["b"], cg.SolverConfig(mode=mode, epsilon=1e-300, max_iterations=a.iters,
-                                                    history_stride=10**9, timing="kernels"))
+                                                    history_stride=10**9, timing="kernels",
+                                                    reduction=a.red, partitions=256))
     print(mode, r.iterations, {k: v for k, v in r.kernel_seconds.items() if v}, flush=True)
