@@ -91,12 +91,15 @@ int mwcg_matrix_create(mwcg_matrix **out, int64_t n_rows, int64_t n_cols, int64_
                        const void *row_ptr, const void *col_idx, const double *values,
                        int index_bytes, void *stream);
 /* row_base: global index of local row 0 (a rank's rows of a partitioned
- * matrix with global columns; 0 otherwise).  col_format: -1 auto (int16
- * column deltas when every |col - row| < 2^15, else int32), 0 int32, 1 int16. */
+ * matrix with global columns; 0 otherwise).  col_format: -1 auto (slice-shared
+ * column offsets when the 32 rows of each slice share them -- stencils, bands
+ * -- else int16 column deltas when every |col - row| < 2^15, else int32),
+ * 0 int32, 1 int16, 2 slice-shared offsets (error if a slice needs more than
+ * its longest row + 2 slots). */
 int mwcg_matrix_create_ex(mwcg_matrix **out, int64_t n_rows, int64_t n_cols, int64_t nnz,
                           const void *row_ptr, const void *col_idx, const double *values,
                           int index_bytes, int64_t row_base, int col_format, void *stream);
-int mwcg_matrix_col_bytes(const mwcg_matrix *A);   /* 2 (int16 deltas) or 4 */
+int mwcg_matrix_col_bytes(const mwcg_matrix *A);   /* 2 (int16 deltas), 4 (int32), 0 (slice-shared) */
 int mwcg_matrix_destroy(mwcg_matrix *A);
 int mwcg_matrix_info(const mwcg_matrix *A, int64_t *n_rows, int64_t *n_cols, int64_t *nnz,
                      int64_t *padded_entries);

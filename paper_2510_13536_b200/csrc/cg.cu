@@ -63,6 +63,7 @@ __device__ void scalar_beta(CgState *st, V<Arith<M>::W> rho_new, cudaGraphCondit
     constexpr int W = Ar::W;
     long long k = st->k + 1;
     st->k = k;
+    st->x_pending = 1;  // K3 applies x += alpha p (cg.py:162) for this iteration
     for (int i = 0; i < W; i++) st->rho_new[i] = rho_new.w[i];
     double rf = Ar::collapse(rho_new);
     double rel = sqrt(fabs(rf)) / st->b_norm;  // rel_residual: cg.py:125-127
@@ -253,16 +254,22 @@ __global__ void __launch_bounds__(SpTraits<M>::THREADS, SpTraits<M>::MINB)
 }
 
 // ---------------------------------------------------------------- K2
+// r += (-alpha) q [norm r], r.r tile partials; last CTA: beta and the stop
+// tests.  The x update (cg.py:162) needs only alpha and the OLD p, so it is
+// deferred to K3, which reads p anyway: K2 streams 3 vector passes (r, q in;
+// r out) instead of 6, and K3 5 instead of 3 -- one p pass fewer per
+// iteration.  Elementwise operations and their inputs are unchanged, so
+// every bit of x is too.
+//
 // Loads are hoisted HOIST elements at a time (all loads of a group issue
-// before any arithmetic; the compiler does not hoist loads of x/r above the
-// stores of the previous element by itself).  TW is FP64-bound: no hoisting,
-// registers go to occupancy instead.
+// before any arithmetic).  TW is FP64-bound: no hoisting, registers go to
+// occupancy instead.
 template <int M>
 struct Hoist {
 #ifdef MWCG_UP_HOIST_OVERRIDE
     static constexpr int value = (M == TW) ? 1 : MWCG_UP_HOIST_OVERRIDE;
 #else
-    static constexpr int value = (M == TW) ? 1 : (Arith<M>::W == 3 ? 2 : TILE_ELEMS);
+    static constexpr int value = (M == TW) ? 1 : TILE_ELEMS;
 #endif
 #ifdef MWCG_UP_MINB_OVERRIDE
     static constexpr int MINB = MWCG_UP_MINB_OVERRIDE;
@@ -275,24 +282,19 @@ struct Hoist {
 
 template <int M, bool FUSED>
 __global__ void __launch_bounds__(TILE_THREADS, Hoist<M>::MINB)
-    cg_update(double *__restrict__ x, double *__restrict__ r, const double *__restrict__ p,
-              const double *__restrict__ q, Geo g, double *__restrict__ part, CgState *st,
-              cudaGraphConditionalHandle h, int use_cond) {
+    cg_update(double *__restrict__ r, const double *__restrict__ q, Geo g, double *__restrict__ part,
+              CgState *st, cudaGraphConditionalHandle h, int use_cond) {
     using Ar = Arith<M>;
     constexpr int W = Ar::W;
     constexpr int H = Hoist<M>::value;
     __shared__ double smem[W * TILE_THREADS / 32];
     __shared__ int s_last;
     if (stopped(st, h, use_cond)) return;
-    const bool norm_all = st->norm_all != 0, norm_r = st->norm_r != 0;
-    V<W> alpha, nalpha;
+    const bool norm_r = st->norm_r != 0;
+    V<W> nalpha;
 #pragma unroll
-    for (int k = 0; k < W; k++) {
-        alpha.w[k] = st->alpha[k];
-        nalpha.w[k] = st->neg_alpha[k];
-    }
+    for (int k = 0; k < W; k++) nalpha.w[k] = st->neg_alpha[k];
     const int64_t n = g.n, ld = g.ld;
-    const double *__restrict__ pl = p + g.p_off * W;  // local slice of p (AoS)
     const int dir = (int)((st->k & 1) ^ 1);
     for (int64_t t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
         const int64_t tile = snake(t, g.ntiles, dir);
@@ -300,13 +302,11 @@ __global__ void __launch_bounds__(TILE_THREADS, Hoist<M>::MINB)
         V<W> acc = zero<W>();
 #pragma unroll
         for (int j0 = 0; j0 < TILE_ELEMS; j0 += H) {
-            V<W> xv[H], pv[H], rv[H], qv[H];
+            V<W> rv[H], qv[H];
 #pragma unroll
             for (int h2 = 0; h2 < H; h2++) {
                 int64_t i = base + (j0 + h2) * TILE_THREADS;
                 if (i < n) {
-                    xv[h2] = load<W>(x, ld, i);
-                    pv[h2] = load_aos_ro<W>(pl, i);
                     rv[h2] = load<W>(r, ld, i);
                     qv[h2] = load_ro<W>(q, ld, i);
                 }
@@ -315,9 +315,6 @@ __global__ void __launch_bounds__(TILE_THREADS, Hoist<M>::MINB)
             for (int h2 = 0; h2 < H; h2++) {
                 int64_t i = base + (j0 + h2) * TILE_THREADS;
                 if (i < n) {
-                    V<W> xi = Ar::add(xv[h2], Ar::mul(alpha, pv[h2]));
-                    if (norm_all) xi = Ar::norm(xi);
-                    store<W>(x, ld, i, xi);
                     V<W> ri = Ar::add(rv[h2], Ar::mul(nalpha, qv[h2]));
                     if (norm_r) ri = Ar::norm(ri);
                     store<W>(r, ld, i, ri);
@@ -340,66 +337,129 @@ __global__ void __launch_bounds__(TILE_THREADS, Hoist<M>::MINB)
 }
 
 // ---------------------------------------------------------------- K3
+// x += alpha p_old [norm x] (cg.py:162-164, deferred from K2) whenever K2 ran
+// this iteration (x_pending, set by scalar_beta) -- also on the iteration
+// that converges or breaks down after the x update, as the reference does --
+// and p = r + beta p [norm p] (cg.py:178-180) while the solve is running.
+// The last CTA clears x_pending.
+__device__ __forceinline__ bool k3_begin(CgState *st, cudaGraphConditionalHandle h, int use_cond, bool &do_p) {
+    if (!st->x_pending) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) set_cond(h, use_cond, 0u);
+        return false;
+    }
+    do_p = !halted(st);
+    if (!do_p && blockIdx.x == 0 && threadIdx.x == 0) set_cond(h, use_cond, 0u);
+    return true;
+}
+
+__device__ __forceinline__ void k3_end(CgState *st, int *s_last) {
+    if (last_block_done(&st->ticket[3], s_last) && threadIdx.x == 0) {
+        st->ticket[3] = 0u;
+        st->x_pending = 0;
+    }
+}
+
+template <int M, bool DO_P>
+__device__ __forceinline__ void k3_element(double *__restrict__ x, double *__restrict__ pl, int64_t ld, int64_t i,
+                                           V<Arith<M>::W> rv, V<Arith<M>::W> pv, V<Arith<M>::W> xv,
+                                           const V<Arith<M>::W> &alpha, const V<Arith<M>::W> &beta,
+                                           bool norm_all) {
+    using Ar = Arith<M>;
+    constexpr int W = Ar::W;
+    V<W> xi = Ar::add(xv, Ar::mul(alpha, pv));
+    if (norm_all) xi = Ar::norm(xi);
+    store<W>(x, ld, i, xi);
+    if (DO_P) {
+        V<W> pi = Ar::add(rv, Ar::mul(beta, pv));
+        if (norm_all) pi = Ar::norm(pi);
+        store_aos<W>(pl, i, pi);
+    }
+}
+
 template <int M>
-__global__ void __launch_bounds__(TILE_THREADS)
-    cg_xpay(double *__restrict__ p, const double *__restrict__ r, Geo g, CgState *st,
+struct XpHoist {
+#ifdef MWCG_XP_HOIST_OVERRIDE
+    static constexpr int value = MWCG_XP_HOIST_OVERRIDE;
+#else
+    static constexpr int value = TILE_ELEMS;
+#endif
+#ifdef MWCG_XP_MINB_OVERRIDE
+    static constexpr int MINB = MWCG_XP_MINB_OVERRIDE;
+#else
+    static constexpr int MINB = 1;
+#endif
+};
+
+template <int M>
+__global__ void __launch_bounds__(TILE_THREADS, XpHoist<M>::MINB)
+    cg_xpay(double *__restrict__ x, double *__restrict__ p, const double *__restrict__ r, Geo g, CgState *st,
             cudaGraphConditionalHandle h, int use_cond) {
     using Ar = Arith<M>;
     constexpr int W = Ar::W;
-    if (stopped(st, h, use_cond)) return;
+    constexpr int H = XpHoist<M>::value;
+    __shared__ int s_last;
+    bool do_p = false;
+    if (!k3_begin(st, h, use_cond, do_p)) return;
     const bool norm_all = st->norm_all != 0;
-    V<W> beta;
+    V<W> alpha, beta;
 #pragma unroll
-    for (int k = 0; k < W; k++) beta.w[k] = st->beta[k];
+    for (int k = 0; k < W; k++) {
+        alpha.w[k] = st->alpha[k];
+        beta.w[k] = st->beta[k];
+    }
     const int64_t n = g.n, ld = g.ld;
     double *__restrict__ pl = p + g.p_off * W;
     const int dir = (int)((st->k & 1) ^ 1);
     for (int64_t t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
         const int64_t tile = snake(t, g.ntiles, dir);
         const int64_t base = tile * TILE + threadIdx.x;
-        V<W> rv[TILE_ELEMS], pv[TILE_ELEMS];
 #pragma unroll
-        for (int j = 0; j < TILE_ELEMS; j++) {
-            int64_t i = base + j * TILE_THREADS;
-            if (i < n) {
-                rv[j] = load_ro<W>(r, ld, i);
-                pv[j] = load_aos<W>(pl, i);
+        for (int j0 = 0; j0 < TILE_ELEMS; j0 += H) {
+            V<W> rv[H], pv[H], xv[H];
+#pragma unroll
+            for (int j = 0; j < H; j++) {
+                int64_t i = base + (j0 + j) * TILE_THREADS;
+                if (i < n) {
+                    if (do_p) rv[j] = load_ro<W>(r, ld, i);
+                    pv[j] = load_aos<W>(pl, i);
+                    xv[j] = load<W>(x, ld, i);
+                }
             }
-        }
 #pragma unroll
-        for (int j = 0; j < TILE_ELEMS; j++) {
-            int64_t i = base + j * TILE_THREADS;
-            if (i < n) {
-                V<W> pi = Ar::add(rv[j], Ar::mul(beta, pv[j]));
-                if (norm_all) pi = Ar::norm(pi);
-                store_aos<W>(pl, i, pi);
+            for (int j = 0; j < H; j++) {
+                int64_t i = base + (j0 + j) * TILE_THREADS;
+                if (i < n) {
+                    if (do_p) k3_element<M, true>(x, pl, ld, i, rv[j], pv[j], xv[j], alpha, beta, norm_all);
+                    else k3_element<M, false>(x, pl, ld, i, rv[j], pv[j], xv[j], alpha, beta, norm_all);
+                }
             }
         }
     }
+    k3_end(st, &s_last);
 }
 
 // ---------------------------------------------------------------- TMA-staged K2 / K3
-// The vector passes are pure streams: each tile's operands (x, r, q word
-// planes, the AoS slice of p) are contiguous 8-KB runs, so one thread issues
-// them as 1-D bulk copies (cp.async.bulk) into a shared-memory ring of NS
-// stages and the copy engine, not registers, holds the bytes in flight.
-// One CTA of TILE_THREADS threads per SM; the canonical tile mapping
-// (thread t: elements t + j*256) and the canonical r.r tree are unchanged,
-// so results are bitwise those of cg_update / cg_xpay.  A partial last tile
-// is read with plain loads (its stage is completed by a plain arrive, so the
-// ring's phase bits stay in step).  Requires 16-B aligned planes (ld even).
+// The vector passes are pure streams: each tile's operands (word planes, the
+// AoS slice of p) are contiguous 8-KB runs, so one thread issues them as 1-D
+// bulk copies (cp.async.bulk) into a shared-memory ring of NS stages and the
+// copy engine, not registers, holds the bytes in flight.  One CTA of
+// TILE_THREADS threads per SM; the canonical tile mapping (thread t: elements
+// t + j*256) and the canonical r.r tree are unchanged, so results are bitwise
+// those of cg_update / cg_xpay.  A partial last tile is read with plain loads
+// (its stage is completed by a plain arrive, so the ring's phase bits stay in
+// step).  Requires 16-B aligned planes (ld even).
 template <int M>
 struct UpTma {
     static constexpr int W = Arith<M>::W;
-    static constexpr int STAGE = 4 * W * TILE;  // doubles: x, r, q planes + p AoS
-    static constexpr int NS = (M == FP64) ? 4 : (W == 2 ? 3 : 2);
+    static constexpr int STAGE = 2 * W * TILE;  // doubles: r, q planes
+    static constexpr int NS = (M == FP64) ? 6 : (W == 2 ? 5 : 4);
     static constexpr size_t SMEM = sizeof(double) * STAGE * NS;
 };
 template <int M>
 struct XpTma {
     static constexpr int W = Arith<M>::W;
-    static constexpr int STAGE = 2 * W * TILE;  // r planes + p AoS
-    static constexpr int NS = (M == FP64) ? 6 : (W == 2 ? 5 : 4);
+    static constexpr int STAGE = 3 * W * TILE;  // r, x planes + p AoS
+    static constexpr int NS = (M == FP64) ? 4 : (W == 2 ? 3 : 2);
     static constexpr size_t SMEM = sizeof(double) * STAGE * NS;
 };
 
@@ -407,32 +467,30 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-template <int M>
-__device__ __forceinline__ void up_issue(double *stage, uint64_t *bar, const double *x, const double *r,
-                                         const double *q, const double *pl, int64_t ld, int64_t tile,
-                                         bool full) {
-    constexpr int W = Arith<M>::W;
+// issue the bulk copies of one tile: NP word-plane groups of W planes
+// (srcs[0..NP-1]) then, if pl, the AoS slice of p; a partial tile arrives
+// without transactions
+template <int W, int NP>
+__device__ __forceinline__ void tile_issue(double *stage, uint64_t *bar, const double *const (&srcs)[NP],
+                                           const double *pl, int64_t ld, int64_t tile, bool full) {
     if (!full) {
         mbar_arrive(bar);
         return;
     }
     constexpr uint32_t PB = TILE * sizeof(double);
-    mbar_arrive_expect_tx(bar, 4u * W * PB);
+    mbar_arrive_expect_tx(bar, (uint32_t)(NP * W + (pl ? W : 0)) * PB);
     const int64_t e0 = tile * TILE;
 #pragma unroll
-    for (int k = 0; k < W; k++) {
-        bulk_g2s(stage + (0 * W + k) * TILE, x + k * ld + e0, PB, bar);
-        bulk_g2s(stage + (1 * W + k) * TILE, r + k * ld + e0, PB, bar);
-        bulk_g2s(stage + (2 * W + k) * TILE, q + k * ld + e0, PB, bar);
-    }
-    bulk_g2s(stage + 3 * W * TILE, pl + e0 * W, W * PB, bar);
+    for (int v = 0; v < NP; v++)
+#pragma unroll
+        for (int k = 0; k < W; k++) bulk_g2s(stage + (v * W + k) * TILE, srcs[v] + k * ld + e0, PB, bar);
+    if (pl) bulk_g2s(stage + NP * W * TILE, pl + e0 * W, W * PB, bar);
 }
 
 template <int M, bool FUSED>
 __global__ void __launch_bounds__(TILE_THREADS, 1)
-    cg_update_tma(double *__restrict__ x, double *__restrict__ r, const double *__restrict__ p,
-                  const double *__restrict__ q, Geo g, double *__restrict__ part, CgState *st,
-                  cudaGraphConditionalHandle h, int use_cond) {
+    cg_update_tma(double *__restrict__ r, const double *__restrict__ q, Geo g, double *__restrict__ part,
+                  CgState *st, cudaGraphConditionalHandle h, int use_cond) {
     using Ar = Arith<M>;
     using T = UpTma<M>;
     constexpr int W = Ar::W;
@@ -441,23 +499,20 @@ __global__ void __launch_bounds__(TILE_THREADS, 1)
     __shared__ double smem[W * TILE_THREADS / 32];
     __shared__ int s_last;
     if (stopped(st, h, use_cond)) return;
-    const bool norm_all = st->norm_all != 0, norm_r = st->norm_r != 0;
-    V<W> alpha, nalpha;
+    const bool norm_r = st->norm_r != 0;
+    V<W> nalpha;
 #pragma unroll
-    for (int k = 0; k < W; k++) {
-        alpha.w[k] = st->alpha[k];
-        nalpha.w[k] = st->neg_alpha[k];
-    }
+    for (int k = 0; k < W; k++) nalpha.w[k] = st->neg_alpha[k];
     const int64_t n = g.n, ld = g.ld;
-    const double *__restrict__ pl = p + g.p_off * W;
     const int dir = (int)((st->k & 1) ^ 1);
     const int64_t nmine = g.ntiles > blockIdx.x ? (g.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const double *const srcs[2] = {r, q};
     if (threadIdx.x == 0) {
         for (int i = 0; i < T::NS; i++) mbar_init(&bar[i], 1);
         mbar_init_fence();
         for (int64_t i = 0; i < T::NS && i < nmine; i++) {
             const int64_t tile = snake(blockIdx.x + i * gridDim.x, g.ntiles, dir);
-            up_issue<M>(ring + i * T::STAGE, &bar[i], x, r, q, pl, ld, tile, (tile + 1) * TILE <= n);
+            tile_issue<W, 2>(ring + i * T::STAGE, &bar[i], srcs, nullptr, ld, tile, (tile + 1) * TILE <= n);
         }
     }
     __syncthreads();
@@ -473,25 +528,18 @@ __global__ void __launch_bounds__(TILE_THREADS, 1)
         for (int j = 0; j < TILE_ELEMS; j++) {
             const int li = threadIdx.x + j * TILE_THREADS;
             const int64_t e = base + j * TILE_THREADS;
-            V<W> xv, pv, rv, qv;
+            V<W> rv, qv;
             if (full) {
 #pragma unroll
                 for (int k = 0; k < W; k++) {
-                    xv.w[k] = sg[(0 * W + k) * TILE + li];
-                    rv.w[k] = sg[(1 * W + k) * TILE + li];
-                    qv.w[k] = sg[(2 * W + k) * TILE + li];
-                    pv.w[k] = sg[3 * W * TILE + li * W + k];
+                    rv.w[k] = sg[(0 * W + k) * TILE + li];
+                    qv.w[k] = sg[(1 * W + k) * TILE + li];
                 }
             } else if (e < n) {
-                xv = load<W>(x, ld, e);
-                pv = load_aos_ro<W>(pl, e);
                 rv = load<W>(r, ld, e);
                 qv = load_ro<W>(q, ld, e);
             }
             if (e < n) {
-                V<W> xi = Ar::add(xv, Ar::mul(alpha, pv));
-                if (norm_all) xi = Ar::norm(xi);
-                store<W>(x, ld, e, xi);
                 V<W> ri = Ar::add(rv, Ar::mul(nalpha, qv));
                 if (norm_r) ri = Ar::norm(ri);
                 store<W>(r, ld, e, ri);
@@ -502,7 +550,7 @@ __global__ void __launch_bounds__(TILE_THREADS, 1)
         if (threadIdx.x == 0 && i + T::NS < nmine) {
             fence_proxy_async_smem();
             const int64_t nt = snake(blockIdx.x + (i + T::NS) * gridDim.x, g.ntiles, dir);
-            up_issue<M>(ring + sidx * T::STAGE, &bar[sidx], x, r, q, pl, ld, nt, (nt + 1) * TILE <= n);
+            tile_issue<W, 2>(ring + sidx * T::STAGE, &bar[sidx], srcs, nullptr, ld, nt, (nt + 1) * TILE <= n);
         }
         if (FUSED) {
             acc = block_tree<M, TILE_THREADS>(acc, smem);
@@ -519,45 +567,35 @@ __global__ void __launch_bounds__(TILE_THREADS, 1)
 }
 
 template <int M>
-__device__ __forceinline__ void xp_issue(double *stage, uint64_t *bar, const double *r, const double *pl,
-                                         int64_t ld, int64_t tile, bool full) {
-    constexpr int W = Arith<M>::W;
-    if (!full) {
-        mbar_arrive(bar);
-        return;
-    }
-    constexpr uint32_t PB = TILE * sizeof(double);
-    mbar_arrive_expect_tx(bar, 2u * W * PB);
-    const int64_t e0 = tile * TILE;
-#pragma unroll
-    for (int k = 0; k < W; k++) bulk_g2s(stage + k * TILE, r + k * ld + e0, PB, bar);
-    bulk_g2s(stage + W * TILE, pl + e0 * W, W * PB, bar);
-}
-
-template <int M>
 __global__ void __launch_bounds__(TILE_THREADS, 1)
-    cg_xpay_tma(double *__restrict__ p, const double *__restrict__ r, Geo g, CgState *st,
+    cg_xpay_tma(double *__restrict__ x, double *__restrict__ p, const double *__restrict__ r, Geo g, CgState *st,
                 cudaGraphConditionalHandle h, int use_cond) {
     using Ar = Arith<M>;
     using T = XpTma<M>;
     constexpr int W = Ar::W;
     extern __shared__ __align__(128) double ring[];
     __shared__ uint64_t bar[T::NS];
-    if (stopped(st, h, use_cond)) return;
+    __shared__ int s_last;
+    bool do_p = false;
+    if (!k3_begin(st, h, use_cond, do_p)) return;
     const bool norm_all = st->norm_all != 0;
-    V<W> beta;
+    V<W> alpha, beta;
 #pragma unroll
-    for (int k = 0; k < W; k++) beta.w[k] = st->beta[k];
+    for (int k = 0; k < W; k++) {
+        alpha.w[k] = st->alpha[k];
+        beta.w[k] = st->beta[k];
+    }
     const int64_t n = g.n, ld = g.ld;
     double *__restrict__ pl = p + g.p_off * W;
     const int dir = (int)((st->k & 1) ^ 1);
     const int64_t nmine = g.ntiles > blockIdx.x ? (g.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const double *const srcs[2] = {r, x};
     if (threadIdx.x == 0) {
         for (int i = 0; i < T::NS; i++) mbar_init(&bar[i], 1);
         mbar_init_fence();
         for (int64_t i = 0; i < T::NS && i < nmine; i++) {
             const int64_t tile = snake(blockIdx.x + i * gridDim.x, g.ntiles, dir);
-            xp_issue<M>(ring + i * T::STAGE, &bar[i], r, pl, ld, tile, (tile + 1) * TILE <= n);
+            tile_issue<W, 2>(ring + i * T::STAGE, &bar[i], srcs, pl, ld, tile, (tile + 1) * TILE <= n);
         }
     }
     __syncthreads();
@@ -572,30 +610,32 @@ __global__ void __launch_bounds__(TILE_THREADS, 1)
         for (int j = 0; j < TILE_ELEMS; j++) {
             const int li = threadIdx.x + j * TILE_THREADS;
             const int64_t e = base + j * TILE_THREADS;
-            V<W> rv, pv;
+            V<W> rv, xv, pv;
             if (full) {
 #pragma unroll
                 for (int k = 0; k < W; k++) {
-                    rv.w[k] = sg[k * TILE + li];
-                    pv.w[k] = sg[W * TILE + li * W + k];
+                    rv.w[k] = sg[(0 * W + k) * TILE + li];
+                    xv.w[k] = sg[(1 * W + k) * TILE + li];
+                    pv.w[k] = sg[2 * W * TILE + li * W + k];
                 }
             } else if (e < n) {
                 rv = load_ro<W>(r, ld, e);
+                xv = load<W>(x, ld, e);
                 pv = load_aos<W>(pl, e);
             }
             if (e < n) {
-                V<W> pi = Ar::add(rv, Ar::mul(beta, pv));
-                if (norm_all) pi = Ar::norm(pi);
-                store_aos<W>(pl, e, pi);
+                if (do_p) k3_element<M, true>(x, pl, ld, e, rv, pv, xv, alpha, beta, norm_all);
+                else k3_element<M, false>(x, pl, ld, e, rv, pv, xv, alpha, beta, norm_all);
             }
         }
         __syncthreads();
         if (threadIdx.x == 0 && i + T::NS < nmine) {
             fence_proxy_async_smem();
             const int64_t nt = snake(blockIdx.x + (i + T::NS) * gridDim.x, g.ntiles, dir);
-            xp_issue<M>(ring + sidx * T::STAGE, &bar[sidx], r, pl, ld, nt, (nt + 1) * TILE <= n);
+            tile_issue<W, 2>(ring + sidx * T::STAGE, &bar[sidx], srcs, pl, ld, nt, (nt + 1) * TILE <= n);
         }
     }
+    k3_end(st, &s_last);
 }
 
 // ---------------------------------------------------------------- init
@@ -808,31 +848,33 @@ template <int M, bool FUSED>
 void launch_k1(mwcg_solver *s, cudaStream_t st, cudaGraphConditionalHandle h, int use_cond) {
     const Geo &g = s->geo;
     const unsigned g0 = s->grid[0];
-    if (s->A.col16)
-        cg_spmv_pq<M, FUSED, int16_t><<<g0, SpTraits<M>::THREADS, 0, st>>>(s->A, s->p, s->q, g, s->part, s->st,
-                                                                           h, use_cond);
-    else
-        cg_spmv_pq<M, FUSED, int32_t><<<g0, SpTraits<M>::THREADS, 0, st>>>(s->A, s->p, s->q, g, s->part, s->st,
-                                                                           h, use_cond);
+#define K1_LAUNCH(CT)                                                                                \
+    cg_spmv_pq<M, FUSED, CT><<<g0, SpTraits<M>::THREADS, 0, st>>>(s->A, s->p, s->q, g, s->part, s->st, h, \
+                                                                  use_cond)
+    if (s->A.dia) K1_LAUNCH(DiaTag);
+    else if (s->A.col16) K1_LAUNCH(int16_t);
+    else K1_LAUNCH(int32_t);
+#undef K1_LAUNCH
 }
 
 template <int M, bool FUSED>
 void launch_k2(mwcg_solver *s, cudaStream_t st, cudaGraphConditionalHandle h, int use_cond) {
     const Geo &g = s->geo;
     if (s->tma)
-        cg_update_tma<M, FUSED><<<s->grid[1], TILE_THREADS, UpTma<M>::SMEM, st>>>(s->x, s->r, s->p, s->q, g,
+        cg_update_tma<M, FUSED><<<s->grid[1], TILE_THREADS, UpTma<M>::SMEM, st>>>(s->r, s->q, g,
                                                                                   s->part, s->st, h, use_cond);
     else
-        cg_update<M, FUSED><<<s->grid[1], TILE_THREADS, 0, st>>>(s->x, s->r, s->p, s->q, g, s->part, s->st, h,
+        cg_update<M, FUSED><<<s->grid[1], TILE_THREADS, 0, st>>>(s->r, s->q, g, s->part, s->st, h,
                                                                  use_cond);
 }
 
 template <int M>
 void launch_k3(mwcg_solver *s, cudaStream_t st, cudaGraphConditionalHandle h, int use_cond) {
     if (s->tma)
-        cg_xpay_tma<M><<<s->grid[2], TILE_THREADS, XpTma<M>::SMEM, st>>>(s->p, s->r, s->geo, s->st, h, use_cond);
+        cg_xpay_tma<M><<<s->grid[2], TILE_THREADS, XpTma<M>::SMEM, st>>>(s->x, s->p, s->r, s->geo, s->st, h,
+                                                                         use_cond);
     else
-        cg_xpay<M><<<s->grid[2], TILE_THREADS, 0, st>>>(s->p, s->r, s->geo, s->st, h, use_cond);
+        cg_xpay<M><<<s->grid[2], TILE_THREADS, 0, st>>>(s->x, s->p, s->r, s->geo, s->st, h, use_cond);
 }
 
 // stage 0: K1 [+ reference p.q], 1: K2 [+ reference r.r], 2: K3
@@ -1068,7 +1110,9 @@ int mwcg_matrix_create_ex(mwcg_matrix **out, int64_t n_rows, int64_t n_cols, int
     return 0;
 }
 
-int mwcg_matrix_col_bytes(const mwcg_matrix *A) { return A ? (A->M->view.col16 ? 2 : 4) : -1; }
+int mwcg_matrix_col_bytes(const mwcg_matrix *A) {
+    return A ? (A->M->view.dia ? 0 : (A->M->view.col16 ? 2 : 4)) : -1;
+}
 
 int mwcg_matrix_destroy(mwcg_matrix *A) {
     if (A) {
@@ -1329,7 +1373,8 @@ int mwcg_solver_start(mwcg_solver *s, const double *b, double b_norm, const doub
 #define START(Mx)                                                                                    \
     do {                                                                                             \
         spread_x0_kernel<words_of(Mx)><<<eb, 256, 0, st>>>(ldp, x0, s->p);                          \
-        if (s->A.col16) spmv_aos_kernel<Mx, int16_t><<<sb, TILE_THREADS, 0, st>>>(s->A, s->p, s->q, s->n); \
+        if (s->A.dia) spmv_aos_kernel<Mx, DiaTag><<<sb, TILE_THREADS, 0, st>>>(s->A, s->p, s->q, s->n);  \
+        else if (s->A.col16) spmv_aos_kernel<Mx, int16_t><<<sb, TILE_THREADS, 0, st>>>(s->A, s->p, s->q, s->n); \
         else spmv_aos_kernel<Mx, int32_t><<<sb, TILE_THREADS, 0, st>>>(s->A, s->p, s->q, s->n);          \
     } while (0)
         switch (s->mode) {
@@ -1484,7 +1529,9 @@ int mwcg_solver_metrics(mwcg_solver *s, double *err, double *true_res) {
     case TW: promote_kernel<TW><<<eb, 256, 0, st>>>(n, s->x, n, s->xt); break;
     default: promote_kernel<QTW><<<eb, 256, 0, st>>>(n, s->x, n, s->xt); break;
     }
-    if (s->A.col16)
+    if (s->A.dia)
+        metrics_vec_kernel<DiaTag><<<eb, TILE_THREADS, 0, st>>>(s->A, s->xt, s->b, s->x_star, s->res, s->diff);
+    else if (s->A.col16)
         metrics_vec_kernel<int16_t><<<eb, TILE_THREADS, 0, st>>>(s->A, s->xt, s->b, s->x_star, s->res, s->diff);
     else
         metrics_vec_kernel<int32_t><<<eb, TILE_THREADS, 0, st>>>(s->A, s->xt, s->b, s->x_star, s->res, s->diff);

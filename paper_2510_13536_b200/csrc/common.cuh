@@ -32,6 +32,15 @@ inline int64_t num_tiles(int64_t n) { return (n + TILE - 1) / TILE; }
 // Column storage: when every |col - (row_base + row)| < 2^15 (stencils,
 // banded matrices) the columns are int16 deltas (2 B/entry instead of 4;
 // sentinel INT16_MIN), otherwise absolute int32 (sentinel -1).
+//
+// Slice-shared offsets ("DIA" slices, chosen at build time when the rows of
+// each slice use (almost) the same column offsets -- stencils, bands): slot k
+// of slice j holds, for all 32 rows, the entry at column offset om_k (one
+// uint64 per slot: int32 offset | 32-lane presence mask << 32).  A row's
+// present slots are its CSR entries in ascending column order, so the
+// left-to-right sum is unchanged; no column array is streamed, and a row's
+// gathers depend only on the (L1-resident, warp-uniform) offset word, not on
+// a column load from HBM.
 constexpr int16_t COL16_SENT = -32768;
 constexpr int32_t COL32_SENT = -1;
 
@@ -43,10 +52,16 @@ struct SellMatrix {
     int64_t total;          // padded entry count
     int64_t row_base;       // global index of local row 0 (row-partitioned ranks)
     int col16;              // 1: int16 deltas, 0: int32 absolute
+    int dia;                // 1: slice-shared offsets (om; no column array)
     const int64_t *slice_ptr;
     const void *cols;
     const double *vals;
+    const uint64_t *om;     // dia: per (slice, k) (lane mask << 32 | uint32 offset)
 };
+
+// Format tag of the slice-shared-offset layout (the column-type template
+// parameter of the walks, next to int16_t / int32_t).
+struct DiaTag {};
 
 // Solver status (cg.py:138-183 reasons)
 enum Status : int { RUNNING = 0, CONVERGED = 1, MAX_ITERS = 2, BREAKDOWN = 3 };
@@ -72,6 +87,7 @@ struct CgState {
     int norm_all;        // every-op normalization
     int pause;           // K1 reached k_stop inside an unrolled graph body:
                          // the rest of the body is skipped (cleared by the host)
+    int x_pending;       // K2 ran this iteration: K3 owes x += alpha p
     unsigned int ticket[4];  // last-block-done counters
     double metrics[4];   // err^2 sum, res^2 sum (collapsed), bnorm_sq, xs_sq
 };

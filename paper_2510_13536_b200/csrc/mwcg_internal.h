@@ -16,9 +16,11 @@ struct SellMatrixOwned {
     int64_t *slice_ptr = nullptr;
     void *cols = nullptr;
     double *vals = nullptr;
+    uint64_t *om = nullptr;  // slice-shared-offset slot words (dia layout)
 };
 
-// col_format: -1 auto (int16 deltas when they fit), 0 force int32, 1 force int16
+// col_format: -1 auto (slice-shared offsets when they pay, else int16 deltas
+// when they fit, else int32), 0 force int32, 1 force int16, 2 force slice-shared
 int sell_create(SellMatrixOwned **out, int64_t n_rows, int64_t n_cols, int64_t nnz,
                 const void *row_ptr, const void *col_idx, const double *values, int index_bytes,
                 int64_t row_base, int col_format, cudaStream_t st);

@@ -192,7 +192,8 @@ int launch_spmv(int mode, const SellMatrix &A, const double *x, int64_t ldx, dou
     if (tiles == 0) return 0;
 #define L(Mx)                                                                                          \
     do {                                                                                               \
-        if (A.col16) spmv_kernel<Mx, int16_t><<<(unsigned)tiles, TILE_THREADS, 0, st>>>(A, x, ldx, y, ldy); \
+        if (A.dia) spmv_kernel<Mx, DiaTag><<<(unsigned)tiles, TILE_THREADS, 0, st>>>(A, x, ldx, y, ldy);   \
+        else if (A.col16) spmv_kernel<Mx, int16_t><<<(unsigned)tiles, TILE_THREADS, 0, st>>>(A, x, ldx, y, ldy); \
         else spmv_kernel<Mx, int32_t><<<(unsigned)tiles, TILE_THREADS, 0, st>>>(A, x, ldx, y, ldy);         \
     } while (0)
     MWCG_DISPATCH(mode, L);

@@ -1,6 +1,7 @@
 // ops.cuh -- per-row / per-element device bodies shared by the operator-level
 // kernels (ops.cu) and the fused CG kernels (cg.cu).
 #pragma once
+#include <type_traits>
 #include "common.cuh"
 
 namespace mwcg {
@@ -36,10 +37,51 @@ struct ColCodec<int32_t> {  // absolute int32 column
     static __device__ __forceinline__ int col(int, int32_t d) { return d; }
 };
 
+// Slice-shared-offset walk: the U slot words (warp-uniform broadcast loads)
+// and the U values issue together; each gather's address depends only on
+// its slot word, so the gathers overlap the value stream.
+template <int M, int U, bool XAOS>
+__device__ __forceinline__ mw::V<mw::Arith<M>::W> spmv_row_dia(const SellMatrix &A,
+                                                               const double *__restrict__ x, int64_t ldx,
+                                                               int64_t row) {
+    using Ar = mw::Arith<M>;
+    constexpr int W = Ar::W;
+    const int64_t sl = row >> 5;
+    const int64_t s0 = __ldg(A.slice_ptr + sl);
+    const int L = (int)((__ldg(A.slice_ptr + sl + 1) - s0) >> 5);
+    const int lane = (int)(row & 31);
+    const int grow = (int)(A.row_base + row);
+    const uint64_t *__restrict__ op = A.om + (s0 >> 5);
+    const double *__restrict__ vp = A.vals + s0 + lane;
+    mw::V<W> s = mw::zero<W>();
+    for (int k0 = 0; k0 < L; k0 += U) {
+        uint64_t om[U];
+        double a[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int64_t kk = min(k0 + u, L - 1);
+            om[u] = __ldg(op + kk);
+            a[u] = ld_stream(vp + kk * SLICE);
+        }
+        bool ok[U];
+        mw::V<W> xv[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            ok[u] = (k0 + u < L) && ((om[u] >> (32 + lane)) & 1u);
+            const int c = ok[u] ? grow + (int)(uint32_t)om[u] : 0;
+            xv[u] = XAOS ? mw::load_aos_ro<W>(x, c) : mw::load_ro<W>(x, ldx, c);
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++)
+            if (ok[u]) s = Ar::add(s, Ar::dxmul(a[u], xv[u]));
+    }
+    return s;
+}
+
 template <int M, int U, typename CT, bool XAOS = false>
-__device__ __forceinline__ mw::V<mw::Arith<M>::W> spmv_row(const SellMatrix &A,
-                                                           const double *__restrict__ x, int64_t ldx,
-                                                           int64_t row) {
+__device__ __forceinline__ mw::V<mw::Arith<M>::W> spmv_row_sell(const SellMatrix &A,
+                                                                const double *__restrict__ x, int64_t ldx,
+                                                                int64_t row) {
     using Ar = mw::Arith<M>;
     constexpr int W = Ar::W;
     const int64_t sl = row >> 5;
@@ -73,7 +115,16 @@ __device__ __forceinline__ mw::V<mw::Arith<M>::W> spmv_row(const SellMatrix &A,
     return s;
 }
 
-// dispatch helper: F<CT>() with the matrix's column type
-#define MWCG_COLS(A, F) ((A).col16 ? F(int16_t) : F(int32_t))
+// one row of y = A x in the matrix's layout
+template <int M, int U, typename CT, bool XAOS = false>
+__device__ __forceinline__ mw::V<mw::Arith<M>::W> spmv_row(const SellMatrix &A,
+                                                           const double *__restrict__ x, int64_t ldx,
+                                                           int64_t row) {
+    if constexpr (std::is_same<CT, DiaTag>::value) return spmv_row_dia<M, U, XAOS>(A, x, ldx, row);
+    else return spmv_row_sell<M, U, CT, XAOS>(A, x, ldx, row);
+}
+
+// dispatch helper: F(CT) with the matrix's format tag / column type
+#define MWCG_COLS(A, F) ((A).dia ? F(DiaTag) : ((A).col16 ? F(int16_t) : F(int32_t)))
 
 }  // namespace mwcg

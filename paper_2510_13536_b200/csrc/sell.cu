@@ -8,6 +8,7 @@
 // the matrix is banded enough.  Row order of entries is preserved, so the
 // per-row left-to-right accumulation (and hence every bit of the result) is
 // unchanged.
+#include <climits>
 #include <cub/cub.cuh>
 #include "common.cuh"
 #include "mwcg_internal.h"
@@ -64,6 +65,116 @@ __global__ void sell_fill_kernel(const I *__restrict__ rp, const I *__restrict__
     }
 }
 
+// ---------------------------------------------------------------------------
+// Slice-shared offsets (common.cuh): one warp per slice walks its 32 rows'
+// CSR entries in lock-step by ascending column offset (warp min over the
+// lanes' heads); every distinct offset becomes one slot with the ballot of
+// the lanes that have it.  Pass 1 counts slots (capped: a slice needing more
+// than cap = Lmax + DIA_SLACK slots marks the matrix as not DIA-friendly);
+// pass 2 writes the slot words and the values.
+// ---------------------------------------------------------------------------
+constexpr int DIA_SLACK = 2;
+
+template <typename I, bool FILL>
+__global__ void dia_walk_kernel(const I *__restrict__ rp, const I *__restrict__ ci, const double *__restrict__ va,
+                                int64_t n_rows, int64_t n_slices, int64_t row_base, int64_t *__restrict__ slice_sz,
+                                const int64_t *__restrict__ slice_ptr, uint64_t *__restrict__ om,
+                                double *__restrict__ vals, unsigned int *__restrict__ reject) {
+    const int64_t sl = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (sl >= n_slices) return;
+    const int64_t r = sl * SLICE + lane;
+    int64_t head = 0, hi = 0;
+    if (r < n_rows) {
+        head = rp[r];
+        hi = rp[r + 1];
+    }
+    int len = (int)(hi - head);
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) len = max(len, __shfl_xor_sync(0xffffffffu, len, off));
+    const int cap = len + DIA_SLACK;
+    const int64_t g = row_base + r;
+    const int64_t s0 = FILL ? slice_ptr[sl] : 0;
+    int k = 0;
+    for (;;) {
+        const int cur = head < hi ? (int)((int64_t)ci[head] - g) : INT_MAX;
+        const int m = __reduce_min_sync(0xffffffffu, cur);
+        if (m == INT_MAX) break;
+        const bool present = cur == m;
+        const unsigned int mask = __ballot_sync(0xffffffffu, present);
+        if (!FILL && k == cap) {  // more distinct offsets than the slice is worth
+            if (lane == 0) atomicOr(reject, 1u);
+            break;
+        }
+        if (FILL) {
+            if (lane == 0) om[(s0 >> 5) + k] = ((uint64_t)mask << 32) | (uint64_t)(uint32_t)m;
+            vals[s0 + (int64_t)k * SLICE + lane] = present ? va[head] : 0.0;
+        }
+        if (present) head++;
+        k++;
+    }
+    if (!FILL && lane == 0) slice_sz[sl] = (int64_t)k * SLICE;
+}
+
+// Try the slice-shared-offset layout: returns 1 (built), 0 (not worth it:
+// more than DIA_SLACK extra slots in some slice, or > 6 % more slots than the
+// padded SELL layout, or offsets beyond int32), or an error code < 0 / > 1.
+template <typename I>
+static int build_dia(SellMatrixOwned *M, const I *rp, const I *ci, const double *va, int64_t sell_total,
+                     bool force, cudaStream_t st) {
+    SellMatrix &A = M->view;
+    if (A.n_slices == 0) return 0;  // no rows: the (empty) SELL layout
+    int64_t *slice_sz = nullptr, *slice_ptr = nullptr;
+    unsigned int *flag = nullptr;
+    MWCG_CUDA(pool_alloc((void **)&slice_sz, sizeof(int64_t) * (A.n_slices + 1), st));
+    MWCG_CUDA(pool_alloc((void **)&flag, sizeof(unsigned int), st));
+    MWCG_CUDA(cudaMemsetAsync(slice_sz, 0, sizeof(int64_t) * (A.n_slices + 1), st));
+    MWCG_CUDA(cudaMemsetAsync(flag, 0, sizeof(unsigned int), st));
+    const unsigned blocks = (unsigned)((A.n_slices * 32 + 255) / 256);
+    dia_walk_kernel<I, false><<<blocks, 256, 0, st>>>(rp, ci, va, A.n_rows, A.n_slices, A.row_base, slice_sz,
+                                                      nullptr, nullptr, nullptr, flag);
+    MWCG_CHECK_LAUNCH();
+    MWCG_CUDA(pool_alloc((void **)&slice_ptr, sizeof(int64_t) * (A.n_slices + 1), st));
+    size_t tmp_bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, slice_sz, slice_ptr, A.n_slices + 1, st);
+    void *tmp = nullptr;
+    MWCG_CUDA(pool_alloc(&tmp, tmp_bytes, st));
+    MWCG_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, slice_sz, slice_ptr, A.n_slices + 1, st));
+    int64_t total = 0;
+    unsigned int reject = 0;
+    MWCG_CUDA(cudaMemcpyAsync(&total, slice_ptr + A.n_slices, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    MWCG_CUDA(cudaMemcpyAsync(&reject, flag, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
+    MWCG_CUDA(cudaStreamSynchronize(st));
+    pool_free(tmp, st);
+    pool_free(slice_sz, st);
+    pool_free(flag, st);
+    if (!force && (reject || total * 100 > sell_total * 106)) {
+        pool_free(slice_ptr, st);
+        return 0;
+    }
+    if (reject) {
+        pool_free(slice_ptr, st);
+        set_error("slice-shared offsets: a slice needs more than Lmax + %d slots", DIA_SLACK);
+        return MWCG_ERR_VALUE;
+    }
+    const size_t ne = (size_t)(total > 0 ? total : 32);
+    MWCG_CUDA(pool_alloc((void **)&M->om, sizeof(uint64_t) * (ne / 32), st));
+    MWCG_CUDA(pool_alloc((void **)&M->vals, sizeof(double) * ne, st));
+    dia_walk_kernel<I, true><<<blocks, 256, 0, st>>>(rp, ci, va, A.n_rows, A.n_slices, A.row_base, nullptr,
+                                                     slice_ptr, M->om, M->vals, nullptr);
+    MWCG_CHECK_LAUNCH();
+    M->slice_ptr = slice_ptr;
+    A.total = total;
+    A.dia = 1;
+    A.col16 = 0;
+    A.slice_ptr = slice_ptr;
+    A.cols = nullptr;
+    A.vals = M->vals;
+    A.om = M->om;
+    MWCG_CUDA(cudaStreamSynchronize(st));
+    return 1;
+}
+
 template <typename I>
 static int build_sell(SellMatrixOwned *M, const I *rp, const I *ci, const double *va, int col_format,
                       cudaStream_t st) {
@@ -97,6 +208,18 @@ static int build_sell(SellMatrixOwned *M, const I *rp, const I *ci, const double
     pool_free(slice_sz, st);
     pool_free(flag, st);
     A.total = total;
+    if (col_format == 2 || col_format < 0) {  // slice-shared offsets when they pay
+        const int64_t *sell_ptr = M->slice_ptr;
+        M->slice_ptr = nullptr;
+        int rc = build_dia<I>(M, rp, ci, va, total, col_format == 2, st);
+        if (rc == 1) {
+            pool_free((void *)sell_ptr, st);
+            return 0;
+        }
+        M->slice_ptr = (int64_t *)sell_ptr;
+        A.total = total;
+        if (rc != 0) return rc;
+    }
     if (col_format == 1 && wide) {
         set_error("column offsets do not fit int16 deltas");
         return MWCG_ERR_VALUE;
@@ -170,6 +293,7 @@ void sell_destroy(SellMatrixOwned *M) {
     pool_free(M->slice_ptr, 0);
     pool_free(M->cols, 0);
     pool_free(M->vals, 0);
+    pool_free(M->om, 0);
     delete M;
 }
 

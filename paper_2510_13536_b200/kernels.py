@@ -115,7 +115,8 @@ class MultiwordVector:
 def device_matrix(A, row_base=0, col_format=-1):
     """SELL-32 device copy of a CsrMatrix, built once and cached on A.
     row_base: global index of row 0 when A holds a rank's rows with global
-    columns (dist.py); col_format: -1 auto / 0 int32 / 1 int16 deltas."""
+    columns (dist.py); col_format: -1 auto / 0 int32 / 1 int16 deltas /
+    2 slice-shared offsets (include/mwcg_cuda.h)."""
     h = getattr(A, "_device", None)
     if h is not None:
         return h

@@ -372,20 +372,22 @@ def test_c2_full_size_iterations_bitwise(mode):
 
 @pytest.mark.parametrize("mode", orc.MODES)
 def test_int16_delta_and_int32_columns_agree(mode):
-    """The two SELL column encodings (int16 deltas / int32 absolute, both
-    with sentinel padding) give the same bits; a matrix with far columns
-    falls back to int32 automatically."""
+    """The three matrix layouts (slice-shared offsets, int16 column deltas,
+    int32 columns) give the same bits; the stencil picks slice-shared
+    offsets automatically and a matrix with far columns falls back to
+    int32."""
     c = problems.config1()
     A = c["A"]
-    A16 = CsrMatrix(A.n_rows, A.n_cols, A.row_ptr, A.col_idx, A.values)
-    A32 = CsrMatrix(A.n_rows, A.n_cols, A.row_ptr, A.col_idx, A.values)
-    assert K.device_matrix(A16).col_bytes() == 2
-    assert K.device_matrix(A32, col_format=0).col_bytes() == 4
+    mats = {f: CsrMatrix(A.n_rows, A.n_cols, A.row_ptr, A.col_idx, A.values) for f in (-1, 1, 0, 2)}
+    assert K.device_matrix(mats[-1]).col_bytes() == 0
+    assert K.device_matrix(mats[1], col_format=1).col_bytes() == 2
+    assert K.device_matrix(mats[0], col_format=0).col_bytes() == 4
+    assert K.device_matrix(mats[2], col_format=2).col_bytes() == 0
     rng = np.random.default_rng(11)
     x = rng.standard_normal((orc.WORDS[mode], A.n_rows))
-    y16 = K.spmv(A16, _vec(mode, x)).planes.cpu().numpy()
-    y32 = K.spmv(A32, _vec(mode, x)).planes.cpu().numpy()
-    assert same_bits(y16, y32) and same_bits(y16, orc.spmv(mode, A, x))
+    ys = [K.spmv(m, _vec(mode, x)).planes.cpu().numpy() for m in mats.values()]
+    want = orc.spmv(mode, A, x)
+    assert all(same_bits(y, want) for y in ys)
     far = random_symmetric(40000, extra_per_row=2, seed=3)
     assert K.device_matrix(far).col_bytes() == 4
     xf = rng.standard_normal((orc.WORDS[mode], far.n_rows))
