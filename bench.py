@@ -278,6 +278,11 @@ def run_ours(a):
 
     # ---- value: device-resident inputs ------------------------------------
     solver = Solver(A, mode)
+    dmat = kernels.device_matrix(A)
+    cb = dmat.col_bytes()
+    layout = {"format": {0: "slice-shared offsets (SELL-32 slices, pattern table)", 2: "SELL-32 int16 deltas",
+                         4: "SELL-32 int32"}[cb],
+              "col_bytes_per_entry": cb, "padded_entries": dmat.padded_entries(), "nnz": nnz}
     with ClockSampler(local) as clk:
         for _ in range(max(3, a.warmup)):
             device_solve(solver)
@@ -319,8 +324,12 @@ def run_ours(a):
                 "kernel": "cg_spmv_pq (SpMV + fused p.q + alpha)",
                 "algorithmic_bytes_per_launch": k1_bytes(n, nnz, w),
                 "launch_us": k1_s * 1e6, "peak_source": hbm_src,
-                "stage_us": {"K1_spmv_pq": k1_s * 1e6, "K2_update_rr": k2_s * 1e6,
-                             "K3_xpay": k3_s * 1e6},
+                "stage_us": {"K1_spmv_pq": k1_s * 1e6, "K2_update_r_rr": k2_s * 1e6,
+                             "K3_xpay_x": k3_s * 1e6},
+                "vector_passes": {"canonical": 9, "implemented": 10,
+                                  "schedule": "K1: p gathered, q written; K2: r, q read, r written; "
+                                              "K3: r, p, x read, p, x written"},
+                "matrix_layout": layout,
                 "iteration": {"us": 1e6 * dt / max(1, iters),
                               "algorithmic_bytes": algorithmic_bytes(n, nnz, w),
                               "achieved_gbs": algorithmic_bytes(n, nnz, w) * iters / dt / 1e9,

@@ -208,14 +208,19 @@ __global__ void __launch_bounds__(SpTraits<M>::THREADS, SpTraits<M>::MINB)
     const int dir = (int)(st->k & 1);
     for (int64_t t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
         const int64_t tile = snake(t, g.ntiles, dir);
+        // the next row's slice words are loaded while this row walks (they
+        // head its dependency chain)
+        SliceWords nsw = slice_words(A, tile * TILE + threadIdx.x);
 #pragma unroll 1
         for (int k = 0; k < RPT; k++) {
             const int li = threadIdx.x + k * NT;  // row inside the tile
             const int64_t row = tile * TILE + li;
+            const SliceWords sw = nsw;
+            if (k + 1 < RPT) nsw = slice_words(A, row + NT);
             V<W> term = zero<W>();
             if (row < n) {
                 // columns are global: p is the full (replicated) vector
-                V<W> sv = spmv_row<M, SpTraits<M>::U, CT, true>(A, p, 0, row);
+                V<W> sv = spmv_row<M, SpTraits<M>::U, CT, true>(A, p, 0, row, sw);
                 if (norm_all) sv = Ar::norm(sv);
                 store<W>(q, g.ld, row, sv);
                 if (FUSED) term = Ar::mul(load_aos_ro<W>(p, g.p_off + row), sv);
@@ -381,12 +386,12 @@ struct XpHoist {
 #ifdef MWCG_XP_HOIST_OVERRIDE
     static constexpr int value = MWCG_XP_HOIST_OVERRIDE;
 #else
-    static constexpr int value = TILE_ELEMS;
+    static constexpr int value = (M == TW) ? 1 : TILE_ELEMS;  // TW: FP64-bound, occupancy first
 #endif
 #ifdef MWCG_XP_MINB_OVERRIDE
     static constexpr int MINB = MWCG_XP_MINB_OVERRIDE;
 #else
-    static constexpr int MINB = 1;
+    static constexpr int MINB = (M == TW) ? 3 : ((M == QTW) ? 2 : 1);
 #endif
 };
 

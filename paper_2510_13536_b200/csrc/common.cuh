@@ -56,7 +56,8 @@ struct SellMatrix {
     const int64_t *slice_ptr;
     const void *cols;
     const double *vals;
-    const uint64_t *om;     // dia: per (slice, k) (lane mask << 32 | uint32 offset)
+    const uint64_t *om;     // dia: pattern table of slot words (lane mask << 32 | uint32 offset);
+                            // slice_ptr then holds descriptors (start/32 | base << 36)
 };
 
 // Format tag of the slice-shared-offset layout (the column-type template

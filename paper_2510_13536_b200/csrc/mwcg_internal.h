@@ -16,7 +16,8 @@ struct SellMatrixOwned {
     int64_t *slice_ptr = nullptr;
     void *cols = nullptr;
     double *vals = nullptr;
-    uint64_t *om = nullptr;  // slice-shared-offset slot words (dia layout)
+    uint64_t *om = nullptr;  // slice-shared-offset pattern table (dia layout)
+    int64_t n_patterns_words = 0;
 };
 
 // col_format: -1 auto (slice-shared offsets when they pay, else int16 deltas

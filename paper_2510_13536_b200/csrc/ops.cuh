@@ -37,21 +37,36 @@ struct ColCodec<int32_t> {  // absolute int32 column
     static __device__ __forceinline__ int col(int, int32_t d) { return d; }
 };
 
+// The two slice words a row's walk starts from (slice_ptr[s], slice_ptr[s+1]:
+// entry offsets, or dia descriptors).  Loading them is the first link of
+// the row's dependency chain, so callers that walk several rows load the
+// next row's words ahead (cg_spmv_pq).  Rows past the last slice clamp to
+// it (their results are discarded).
+struct SliceWords {
+    int64_t w0, w1;
+};
+__device__ __forceinline__ SliceWords slice_words(const SellMatrix &A, int64_t row) {
+    const int64_t sl = min(row >> 5, A.n_slices - 1);
+    return SliceWords{__ldg(A.slice_ptr + sl), __ldg(A.slice_ptr + sl + 1)};
+}
+
 // Slice-shared-offset walk: the U slot words (warp-uniform broadcast loads)
 // and the U values issue together; each gather's address depends only on
 // its slot word, so the gathers overlap the value stream.
 template <int M, int U, bool XAOS>
 __device__ __forceinline__ mw::V<mw::Arith<M>::W> spmv_row_dia(const SellMatrix &A,
                                                                const double *__restrict__ x, int64_t ldx,
-                                                               int64_t row) {
+                                                               int64_t row, SliceWords sw) {
     using Ar = mw::Arith<M>;
     constexpr int W = Ar::W;
-    const int64_t sl = row >> 5;
-    const int64_t s0 = __ldg(A.slice_ptr + sl);
-    const int L = (int)((__ldg(A.slice_ptr + sl + 1) - s0) >> 5);
+    // slice descriptor: (start / 32) | (pattern base << 36)  (sell.cu: dia_patterns)
+    constexpr uint64_t LO = (1ull << 36) - 1;
+    const uint64_t d0 = (uint64_t)sw.w0, d1 = (uint64_t)sw.w1;
+    const int64_t s0 = (int64_t)(d0 & LO) << 5;
+    const int L = (int)((d1 & LO) - (d0 & LO));
     const int lane = (int)(row & 31);
     const int grow = (int)(A.row_base + row);
-    const uint64_t *__restrict__ op = A.om + (s0 >> 5);
+    const uint64_t *__restrict__ op = A.om + (d0 >> 36);
     const double *__restrict__ vp = A.vals + s0 + lane;
     mw::V<W> s = mw::zero<W>();
     for (int k0 = 0; k0 < L; k0 += U) {
@@ -81,12 +96,11 @@ __device__ __forceinline__ mw::V<mw::Arith<M>::W> spmv_row_dia(const SellMatrix 
 template <int M, int U, typename CT, bool XAOS = false>
 __device__ __forceinline__ mw::V<mw::Arith<M>::W> spmv_row_sell(const SellMatrix &A,
                                                                 const double *__restrict__ x, int64_t ldx,
-                                                                int64_t row) {
+                                                                int64_t row, SliceWords sw) {
     using Ar = mw::Arith<M>;
     constexpr int W = Ar::W;
-    const int64_t sl = row >> 5;
-    const int64_t s0 = __ldg(A.slice_ptr + sl);
-    const int L = (int)((__ldg(A.slice_ptr + sl + 1) - s0) >> 5);
+    const int64_t s0 = sw.w0;
+    const int L = (int)((sw.w1 - s0) >> 5);
     const int64_t off = s0 + (row & 31);
     const int grow = (int)(A.row_base + row);  // n_cols < 2^31 (sell.cu)
     const CT *__restrict__ cp = (const CT *)A.cols + off;
@@ -119,9 +133,15 @@ __device__ __forceinline__ mw::V<mw::Arith<M>::W> spmv_row_sell(const SellMatrix
 template <int M, int U, typename CT, bool XAOS = false>
 __device__ __forceinline__ mw::V<mw::Arith<M>::W> spmv_row(const SellMatrix &A,
                                                            const double *__restrict__ x, int64_t ldx,
+                                                           int64_t row, SliceWords sw) {
+    if constexpr (std::is_same<CT, DiaTag>::value) return spmv_row_dia<M, U, XAOS>(A, x, ldx, row, sw);
+    else return spmv_row_sell<M, U, CT, XAOS>(A, x, ldx, row, sw);
+}
+template <int M, int U, typename CT, bool XAOS = false>
+__device__ __forceinline__ mw::V<mw::Arith<M>::W> spmv_row(const SellMatrix &A,
+                                                           const double *__restrict__ x, int64_t ldx,
                                                            int64_t row) {
-    if constexpr (std::is_same<CT, DiaTag>::value) return spmv_row_dia<M, U, XAOS>(A, x, ldx, row);
-    else return spmv_row_sell<M, U, CT, XAOS>(A, x, ldx, row);
+    return spmv_row<M, U, CT, XAOS>(A, x, ldx, row, slice_words(A, row));
 }
 
 // dispatch helper: F(CT) with the matrix's format tag / column type

@@ -8,7 +8,10 @@
 // the matrix is banded enough.  Row order of entries is preserved, so the
 // per-row left-to-right accumulation (and hence every bit of the result) is
 // unchanged.
+#include <algorithm>
 #include <climits>
+#include <unordered_map>
+#include <vector>
 #include <cub/cub.cuh>
 #include "common.cuh"
 #include "mwcg_internal.h"
@@ -116,6 +119,57 @@ __global__ void dia_walk_kernel(const I *__restrict__ rp, const I *__restrict__ 
     if (!FILL && lane == 0) slice_sz[sl] = (int64_t)k * SLICE;
 }
 
+// Slot-word patterns: stencil and band slices repeat a handful of (offset,
+// mask) sequences (interior / boundary combinations), so the slot words are
+// deduplicated into a pattern table small enough to stay in L1, and each
+// slice's descriptor packs its value offset with its pattern base:
+//   desc[j] = (slice_start / 32) | (pattern_base << 36),
+// desc[n_slices] = total / 32.  A row's gathers then wait on one L2 load
+// (desc) and one L1 hit (the pattern word) instead of two L2 loads.
+static int dia_patterns(SellMatrixOwned *M, int64_t *slice_ptr, int64_t n_words, cudaStream_t st) {
+    SellMatrix &A = M->view;
+    const int64_t ns = A.n_slices;
+    std::vector<int64_t> sp(ns + 1);
+    std::vector<uint64_t> om(n_words);
+    MWCG_CUDA(cudaMemcpyAsync(sp.data(), slice_ptr, sizeof(int64_t) * (ns + 1), cudaMemcpyDeviceToHost, st));
+    MWCG_CUDA(cudaMemcpyAsync(om.data(), M->om, sizeof(uint64_t) * n_words, cudaMemcpyDeviceToHost, st));
+    MWCG_CUDA(cudaStreamSynchronize(st));
+    std::vector<uint64_t> pat;
+    std::vector<uint64_t> desc(ns + 1);
+    std::unordered_multimap<uint64_t, int64_t> seen;  // hash -> pattern base
+    for (int64_t j = 0; j < ns; j++) {
+        const int64_t b = sp[j] >> 5, len = (sp[j + 1] - sp[j]) >> 5;
+        uint64_t hsh = 1469598103934665603ull ^ (uint64_t)len;
+        for (int64_t k = 0; k < len; k++) hsh = (hsh ^ om[b + k]) * 1099511628211ull;
+        int64_t base = -1;
+        auto rng = seen.equal_range(hsh);
+        for (auto it = rng.first; it != rng.second && base < 0; ++it)
+            if (it->second + len <= (int64_t)pat.size() &&
+                std::equal(om.begin() + b, om.begin() + b + len, pat.begin() + it->second))
+                base = it->second;
+        if (base < 0) {
+            base = (int64_t)pat.size();
+            pat.insert(pat.end(), om.begin() + b, om.begin() + b + len);
+            seen.emplace(hsh, base);
+        }
+        if (base >= (1ll << 28)) {
+            set_error("slice-shared offsets: pattern table too large");
+            return MWCG_ERR_VALUE;
+        }
+        desc[j] = (uint64_t)(sp[j] >> 5) | ((uint64_t)base << 36);
+    }
+    desc[ns] = (uint64_t)(sp[ns] >> 5);
+    if (pat.empty()) pat.push_back(0);
+    pool_free(M->om, st);
+    M->om = nullptr;
+    MWCG_CUDA(pool_alloc((void **)&M->om, sizeof(uint64_t) * pat.size(), st));
+    MWCG_CUDA(cudaMemcpyAsync(M->om, pat.data(), sizeof(uint64_t) * pat.size(), cudaMemcpyHostToDevice, st));
+    MWCG_CUDA(cudaMemcpyAsync(slice_ptr, desc.data(), sizeof(uint64_t) * (ns + 1), cudaMemcpyHostToDevice, st));
+    MWCG_CUDA(cudaStreamSynchronize(st));
+    M->n_patterns_words = (int64_t)pat.size();
+    return 0;
+}
+
 // Try the slice-shared-offset layout: returns 1 (built), 0 (not worth it:
 // more than DIA_SLACK extra slots in some slice, or > 6 % more slots than the
 // padded SELL layout, or offsets beyond int32), or an error code < 0 / > 1.
@@ -163,6 +217,8 @@ static int build_dia(SellMatrixOwned *M, const I *rp, const I *ci, const double 
     dia_walk_kernel<I, true><<<blocks, 256, 0, st>>>(rp, ci, va, A.n_rows, A.n_slices, A.row_base, nullptr,
                                                      slice_ptr, M->om, M->vals, nullptr);
     MWCG_CHECK_LAUNCH();
+    int rc = dia_patterns(M, slice_ptr, (int64_t)(ne / 32), st);
+    if (rc) return rc;
     M->slice_ptr = slice_ptr;
     A.total = total;
     A.dia = 1;
