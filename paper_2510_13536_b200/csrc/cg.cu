@@ -1008,9 +1008,15 @@ int compute_grids_t(mwcg_solver *s) {
         MWCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb[2], cg_xpay_tma<M>, TILE_THREADS,
                                                                 XpTma<M>::SMEM));
     }
+    // bit i of `full` -> kernel i (K1, K2, K3, init) gets one CTA per tile
+    // (hardware-balanced) instead of a persistent grid: measured faster for
+    // the compute-heavy TW kernels (C2: 495 -> 466 us/it) and for QTW's K1,
+    // slower for the streaming ones; MWCG_GRID_FULL=<mask> overrides
+    unsigned full = (M == TW) ? 7u : ((M == QTW) ? 1u : 0u);
+    if (const char *t = std::getenv("MWCG_GRID_FULL")) full = (unsigned)std::atoi(t);
     for (int i = 0; i < 4; i++) {
         int64_t g = (int64_t)(nb[i] > 0 ? nb[i] : 1) * sms;
-        if (g > s->geo.ntiles) g = s->geo.ntiles;
+        if (g > s->geo.ntiles || ((full >> i) & 1u)) g = s->geo.ntiles;
         s->grid[i] = (unsigned)(g > 0 ? g : 1);
     }
     return 0;
