@@ -50,13 +50,21 @@ __device__ __forceinline__ SliceWords slice_words(const SellMatrix &A, int64_t r
     return SliceWords{__ldg(A.slice_ptr + sl), __ldg(A.slice_ptr + sl + 1)};
 }
 
-// Slice-shared-offset walk: the U slot words (warp-uniform broadcast loads)
-// and the U values issue together; each gather's address depends only on
-// its slot word, so the gathers overlap the value stream.
+// Slice-shared-offset walk: the U slot words (warp-uniform broadcast loads
+// from the L1-resident pattern table) and the U values issue together; each
+// gather's address depends only on its slot word, so the gathers overlap the
+// value stream.  Every pattern in the table is followed by DIA_PAD zero words
+// and the value array by DIA_PAD slots, so a chunk reads past the slice's
+// last slot without clamping: those slots have an empty lane mask.  A lane
+// without an entry in a slot gathers its own row (always in bounds) and
+// skips the arithmetic.
+constexpr int DIA_PAD = 8;  // >= the largest U
+
 template <int M, int U, bool XAOS>
 __device__ __forceinline__ mw::V<mw::Arith<M>::W> spmv_row_dia(const SellMatrix &A,
                                                                const double *__restrict__ x, int64_t ldx,
                                                                int64_t row, SliceWords sw) {
+    static_assert(U <= DIA_PAD, "pattern padding must cover a chunk");
     using Ar = mw::Arith<M>;
     constexpr int W = Ar::W;
     // slice descriptor: (start / 32) | (pattern base << 36)  (sell.cu: dia_patterns)
@@ -69,21 +77,20 @@ __device__ __forceinline__ mw::V<mw::Arith<M>::W> spmv_row_dia(const SellMatrix 
     const uint64_t *__restrict__ op = A.om + (d0 >> 36);
     const double *__restrict__ vp = A.vals + s0 + lane;
     mw::V<W> s = mw::zero<W>();
-    for (int k0 = 0; k0 < L; k0 += U) {
+    for (int k0 = 0; k0 < L; k0 += U, op += U, vp += U * SLICE) {
         uint64_t om[U];
         double a[U];
 #pragma unroll
         for (int u = 0; u < U; u++) {
-            const int64_t kk = min(k0 + u, L - 1);
-            om[u] = __ldg(op + kk);
-            a[u] = ld_stream(vp + kk * SLICE);
+            om[u] = __ldg(op + u);
+            a[u] = ld_stream(vp + u * SLICE);
         }
         bool ok[U];
         mw::V<W> xv[U];
 #pragma unroll
         for (int u = 0; u < U; u++) {
-            ok[u] = (k0 + u < L) && ((om[u] >> (32 + lane)) & 1u);
-            const int c = ok[u] ? grow + (int)(uint32_t)om[u] : 0;
+            ok[u] = (uint32_t)(om[u] >> 32) & (1u << lane);
+            const int c = grow + (ok[u] ? (int)(uint32_t)om[u] : 0);
             xv[u] = XAOS ? mw::load_aos_ro<W>(x, c) : mw::load_ro<W>(x, ldx, c);
         }
 #pragma unroll

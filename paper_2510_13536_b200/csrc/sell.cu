@@ -15,6 +15,7 @@
 #include <cub/cub.cuh>
 #include "common.cuh"
 #include "mwcg_internal.h"
+#include "ops.cuh"
 
 namespace mwcg {
 
@@ -136,7 +137,7 @@ static int dia_patterns(SellMatrixOwned *M, int64_t *slice_ptr, int64_t n_words,
     MWCG_CUDA(cudaStreamSynchronize(st));
     std::vector<uint64_t> pat;
     std::vector<uint64_t> desc(ns + 1);
-    std::unordered_multimap<uint64_t, int64_t> seen;  // hash -> pattern base
+    std::unordered_multimap<uint64_t, std::pair<int64_t, int64_t>> seen;  // hash -> (pattern base, length)
     for (int64_t j = 0; j < ns; j++) {
         const int64_t b = sp[j] >> 5, len = (sp[j + 1] - sp[j]) >> 5;
         uint64_t hsh = 1469598103934665603ull ^ (uint64_t)len;
@@ -144,13 +145,14 @@ static int dia_patterns(SellMatrixOwned *M, int64_t *slice_ptr, int64_t n_words,
         int64_t base = -1;
         auto rng = seen.equal_range(hsh);
         for (auto it = rng.first; it != rng.second && base < 0; ++it)
-            if (it->second + len <= (int64_t)pat.size() &&
-                std::equal(om.begin() + b, om.begin() + b + len, pat.begin() + it->second))
-                base = it->second;
+            if (it->second.second == len &&
+                std::equal(om.begin() + b, om.begin() + b + len, pat.begin() + it->second.first))
+                base = it->second.first;
         if (base < 0) {
             base = (int64_t)pat.size();
             pat.insert(pat.end(), om.begin() + b, om.begin() + b + len);
-            seen.emplace(hsh, base);
+            pat.insert(pat.end(), DIA_PAD, 0ull);  // empty slots: chunks may read past the end
+            seen.emplace(hsh, std::make_pair(base, len));
         }
         if (base >= (1ll << 28)) {
             set_error("slice-shared offsets: pattern table too large");
@@ -159,7 +161,7 @@ static int dia_patterns(SellMatrixOwned *M, int64_t *slice_ptr, int64_t n_words,
         desc[j] = (uint64_t)(sp[j] >> 5) | ((uint64_t)base << 36);
     }
     desc[ns] = (uint64_t)(sp[ns] >> 5);
-    if (pat.empty()) pat.push_back(0);
+    if (pat.empty()) pat.assign(DIA_PAD, 0ull);
     pool_free(M->om, st);
     M->om = nullptr;
     MWCG_CUDA(pool_alloc((void **)&M->om, sizeof(uint64_t) * pat.size(), st));
@@ -213,7 +215,9 @@ static int build_dia(SellMatrixOwned *M, const I *rp, const I *ci, const double 
     }
     const size_t ne = (size_t)(total > 0 ? total : 32);
     MWCG_CUDA(pool_alloc((void **)&M->om, sizeof(uint64_t) * (ne / 32), st));
-    MWCG_CUDA(pool_alloc((void **)&M->vals, sizeof(double) * ne, st));
+    // DIA_PAD slots of slack: a chunk of the last slice reads past its end
+    MWCG_CUDA(pool_alloc((void **)&M->vals, sizeof(double) * (ne + DIA_PAD * SLICE), st));
+    MWCG_CUDA(cudaMemsetAsync(M->vals + ne, 0, sizeof(double) * DIA_PAD * SLICE, st));
     dia_walk_kernel<I, true><<<blocks, 256, 0, st>>>(rp, ci, va, A.n_rows, A.n_slices, A.row_base, nullptr,
                                                      slice_ptr, M->om, M->vals, nullptr);
     MWCG_CHECK_LAUNCH();
