@@ -312,7 +312,7 @@ def run_ours(a):
     k2_s = pres.stage_ms[1] * 1e-3 / it_p
     k3_s = pres.stage_ms[2] * 1e-3 / it_p
     k1_achieved = k1_bytes(n, nnz, w) / k1_s / 1e9
-    traffic = None
+    traffic, prof = None, {}
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
             prof = json.load(f)
@@ -362,6 +362,13 @@ def run_ours(a):
                       "hbm_gbs": bw, "hbm_frac": hfrac, "fp64_tops": fl / 1e12,
                       "fp64_frac": ffrac, "roofline_frac": max(hfrac, ffrac),
                       "bound": "fp64" if ffrac > hfrac else "hbm"}
+            # FP64-pipe utilisation of the three kernels from the committed ncu
+            # launch list (profiles/ncu_summary.json): the instruction-level
+            # view of the FP64 roofline (counted ops exclude the compares and
+            # selects the exact TW merge needs)
+            pipe = prof.get("fp64_pipe_pct", {}).get(a.config, {}).get(m)
+            if pipe:
+                per[m]["ncu_fp64_pipe_pct"] = pipe
             if sv is not solver:
                 del sv
             torch.cuda.empty_cache()

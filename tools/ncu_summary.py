@@ -64,9 +64,44 @@ def launches_agg(path, command, note):
     return {"command": command, "note": note, "per_kernel": agg, "launches": ls}
 
 
+def k1_summary(path, cfg, source):
+    """Per-mode medians of the fused kernels from a launch list of
+    tools/prof_c2.py --modes fp64,dw,qdw,tw,qtw (one mode after another):
+    K1 DRAM bytes per launch (bench.py roofline.traffic) and FP64-pipe
+    utilisation of K1/K2/K3."""
+    import statistics
+    ls = launches(path)
+    modes = ["fp64", "dw", "qdw", "tw", "qtw"]
+    out = {"source": source, "k1_dram_bytes_per_launch": {cfg: {}}, "fp64_pipe_pct": {cfg: {}},
+           "k1_us": {cfg: {}}}
+    for k, kname in ((0, "cg_spmv_pq"), (1, "cg_update"), (2, "cg_xpay")):
+        per = {}
+        for e in ls:
+            if kname not in e["kernel"]:
+                continue
+            m = modes[int(e["kernel"].split("<")[1].split(",")[0].split(">")[0])]
+            per.setdefault(m, []).append(e)
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1.0, "ns": 1e-3, "us": 1.0,
+                 "msecond": 1e3, "%": 1.0}
+        def val(x, key):
+            v, _, u = x[key].partition(" ")
+            return float(v.replace(",", "")) * scale.get(u.strip(), 1.0)
+        for m, es in per.items():
+            es = es[1:] if len(es) > 2 else es
+            f = lambda key: statistics.median(val(x, key) for x in es if key in x)
+            out["fp64_pipe_pct"][cfg].setdefault(m, {})[kname] = f(
+                "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active")
+            if k == 0:
+                out["k1_dram_bytes_per_launch"][cfg][m] = f("dram__bytes_read.sum") + f("dram__bytes_write.sum")
+                out["k1_us"][cfg][m] = f("gpu__time_duration.sum")
+    return out
+
+
 if __name__ == "__main__":
     kind, src, dst = sys.argv[1:4]
-    if kind == "launches-agg":
+    if kind == "k1-summary":
+        obj = k1_summary(src, sys.argv[4], sys.argv[5])
+    elif kind == "launches-agg":
         obj = launches_agg(src, sys.argv[4], sys.argv[5] if len(sys.argv) > 5 else "")
     else:
         obj = report(src) if kind == "report" else launches(src)
