@@ -143,6 +143,17 @@ class Solver:
         return res, hist
 
 
+_POOL = None
+
+
+def _host_pool():
+    global _POOL
+    if _POOL is None:
+        from concurrent.futures import ThreadPoolExecutor
+        _POOL = ThreadPoolExecutor(max_workers=1, thread_name_prefix="mwcg-host")
+    return _POOL
+
+
 def _b_norm(b):
     out = ctypes.c_double()
     _lib.check(_lib.load().mwcg_norm2_host(b.ctypes.data_as(_lib.c_dp), b.size, ctypes.byref(out)))
@@ -157,6 +168,10 @@ def cg_solve(A, b, config=SolverConfig(), x0=None, x_star=None, reference=False)
     if b.size != A.n_rows:
         raise ValueError("right-hand side length does not match the matrix")
     t0 = time.perf_counter()
+    # ||b|| is a sequential host sum (the reference order, kernels.py:290-296);
+    # it runs on a host thread (ctypes drops the GIL) while the matrix and
+    # solver are set up on the device
+    bn_future = _host_pool().submit(_b_norm, b)
     mode = config.mode
     n = A.n_rows
     reduction = "partitions" if reference else config.reduction
@@ -176,7 +191,7 @@ def cg_solve(A, b, config=SolverConfig(), x0=None, x_star=None, reference=False)
     b_dev = _dev_f64(b)
     x0_dev = None if x0 is None else _dev_f64(np.asarray(x0, dtype=np.float64).reshape(-1))
     xs_dev = None if x_star is None else _dev_f64(np.asarray(x_star, dtype=np.float64).reshape(-1))
-    bn = _b_norm(b)
+    bn = bn_future.result()
     profile = config.timing == "kernels"
     res, hist = solver.solve(b_dev, bn, x0_dev, xs_dev, config.epsilon, config.max_iterations,
                              config.history_stride, profile)
@@ -187,8 +202,8 @@ def cg_solve(A, b, config=SolverConfig(), x0=None, x_star=None, reference=False)
           "normalize": 0.0}
     if profile:
         ks["spmv"] = res.stage_ms[0] * 1e-3      # SpMV + fused p.q (+ alpha)
-        ks["axpy"] = res.stage_ms[1] * 1e-3      # x, r updates + normalize + r.r (+ beta)
-        ks["scal_add"] = res.stage_ms[2] * 1e-3  # p = r + beta p
+        ks["axpy"] = res.stage_ms[1] * 1e-3      # r update + normalize + r.r (+ beta)
+        ks["scal_add"] = res.stage_ms[2] * 1e-3  # x update (deferred axpy) + p = r + beta p
     reason = _lib.STATUS[res.status]
     return SolverResult(converged=reason == "converged", reason=reason,
                         iterations=int(res.iterations),

@@ -457,14 +457,24 @@ template <int M>
 struct UpTma {
     static constexpr int W = Arith<M>::W;
     static constexpr int STAGE = 2 * W * TILE;  // doubles: r, q planes
-    static constexpr int NS = (M == FP64) ? 6 : (W == 2 ? 5 : 4);
+#ifdef MWCG_UP_NS
+    static constexpr int NS = MWCG_UP_NS;
+#else
+    // 2 stages: 2-3 CTAs per SM (measured better than a deeper ring in one CTA:
+    // the per-tile r.r tree needs the extra warps)
+    static constexpr int NS = 2;
+#endif
     static constexpr size_t SMEM = sizeof(double) * STAGE * NS;
 };
 template <int M>
 struct XpTma {
     static constexpr int W = Arith<M>::W;
     static constexpr int STAGE = 3 * W * TILE;  // r, x planes + p AoS
+#ifdef MWCG_XP_NS
+    static constexpr int NS = MWCG_XP_NS;
+#else
     static constexpr int NS = (M == FP64) ? 4 : (W == 2 ? 3 : 2);
+#endif
     static constexpr size_t SMEM = sizeof(double) * STAGE * NS;
 };
 
@@ -841,7 +851,8 @@ struct mwcg_solver {
     unsigned grid[4] = {1, 1, 1, 1};  // spmv_pq, update, xpay, init
     Geo geo{};
     bool dist = false;                   // rank of a row partition (no graph; see dist.py)
-    bool tma = false;                    // TMA-staged K2/K3 (aligned planes; MWCG_TMA=0 disables)
+    bool tma = false;                    // TMA-staged K3 (aligned planes; MWCG_TMA=0/1 overrides)
+    bool tma2 = false;                   // TMA-staged K2 (MWCG_TMA2=0/1 overrides)
 };
 
 namespace {
@@ -865,7 +876,7 @@ void launch_k1(mwcg_solver *s, cudaStream_t st, cudaGraphConditionalHandle h, in
 template <int M, bool FUSED>
 void launch_k2(mwcg_solver *s, cudaStream_t st, cudaGraphConditionalHandle h, int use_cond) {
     const Geo &g = s->geo;
-    if (s->tma)
+    if (s->tma2)
         cg_update_tma<M, FUSED><<<s->grid[1], TILE_THREADS, UpTma<M>::SMEM, st>>>(s->r, s->q, g,
                                                                                   s->part, s->st, h, use_cond);
     else
@@ -976,6 +987,8 @@ int compute_grids_t(mwcg_solver *s) {
         // and TW; MWCG_TMA=0/1 overrides
         const char *t = std::getenv("MWCG_TMA");
         s->tma = t ? t[0] != '0' : (M == QTW);
+        const char *t2 = std::getenv("MWCG_TMA2");
+        s->tma2 = t2 ? t2[0] != '0' : (M != FP64 && M != TW);
     }
     if (s->fused) {
         MWCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb[0], cg_spmv_pq<M, true, int32_t>,
@@ -989,22 +1002,26 @@ int compute_grids_t(mwcg_solver *s) {
         MWCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb[3], cg_init<M, false>, TILE_THREADS, 0));
     }
     MWCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb[2], cg_xpay<M>, TILE_THREADS, 0));
-    if (s->tma) {
+    {
         // alignment of every plane the bulk copies touch (16 B)
         const int W = Arith<M>::W;
         auto al = [](const void *ptr) { return ((uintptr_t)ptr & 15u) == 0; };
-        s->tma = al(s->x) && al(s->r) && al(s->q) && al(s->p) && (s->geo.ld % 2 == 0) &&
-                 ((s->geo.p_off * W) % 2 == 0);
+        const bool ok = al(s->x) && al(s->r) && al(s->q) && al(s->p) && (s->geo.ld % 2 == 0) &&
+                        ((s->geo.p_off * W) % 2 == 0);
+        s->tma = s->tma && ok;
+        s->tma2 = s->tma2 && ok;
     }
-    if (s->tma) {
+    if (s->tma2) {
         MWCG_CUDA(cudaFuncSetAttribute(cg_update_tma<M, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)UpTma<M>::SMEM));
         MWCG_CUDA(cudaFuncSetAttribute(cg_update_tma<M, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)UpTma<M>::SMEM));
-        MWCG_CUDA(cudaFuncSetAttribute(cg_xpay_tma<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)XpTma<M>::SMEM));
         MWCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb[1], cg_update_tma<M, true>, TILE_THREADS,
                                                                 UpTma<M>::SMEM));
+    }
+    if (s->tma) {
+        MWCG_CUDA(cudaFuncSetAttribute(cg_xpay_tma<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)XpTma<M>::SMEM));
         MWCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb[2], cg_xpay_tma<M>, TILE_THREADS,
                                                                 XpTma<M>::SMEM));
     }
