@@ -199,7 +199,11 @@ __global__ void __launch_bounds__(SpTraits<M>::THREADS, SpTraits<M>::MINB)
     constexpr int W = Ar::W;
     constexpr int NT = SpTraits<M>::THREADS;
     constexpr int RPT = SpTraits<M>::RPT;
-    __shared__ double terms[FUSED ? W * TILE : 1];
+    // 256 threads: thread t owns rows t + 256 j, which IS the canonical tile
+    // mapping, so its p.q terms accumulate in registers in canonical order;
+    // 512 threads (FP64) stage the terms in shared memory for the first 256
+    constexpr bool STAGE = FUSED && NT != TILE_THREADS;
+    __shared__ double terms[STAGE ? W * TILE : 1];
     __shared__ double smem[W * TILE_THREADS / 32];
     __shared__ int s_last;
     if (stopped_k1(st, h, use_cond)) return;
@@ -211,6 +215,7 @@ __global__ void __launch_bounds__(SpTraits<M>::THREADS, SpTraits<M>::MINB)
         // the next row's slice words are loaded while this row walks (they
         // head its dependency chain)
         SliceWords nsw = slice_words(A, tile * TILE + threadIdx.x);
+        V<W> acc = zero<W>();
 #pragma unroll 1
         for (int k = 0; k < RPT; k++) {
             const int li = threadIdx.x + k * NT;  // row inside the tile
@@ -224,15 +229,15 @@ __global__ void __launch_bounds__(SpTraits<M>::THREADS, SpTraits<M>::MINB)
                 if (norm_all) sv = Ar::norm(sv);
                 store<W>(q, g.ld, row, sv);
                 if (FUSED) term = Ar::mul(load_aos_ro<W>(p, g.p_off + row), sv);
+                if (FUSED && !STAGE) acc = Ar::add(acc, term);
             }
-            if (FUSED) {
+            if (STAGE) {
 #pragma unroll
                 for (int w = 0; w < W; w++) terms[w * TILE + li] = term.w[w];
             }
         }
-        if (FUSED) {
+        if (STAGE) {
             __syncthreads();
-            V<W> acc = zero<W>();
             if (threadIdx.x < TILE_THREADS) {
                 const int64_t base = tile * TILE + threadIdx.x;
 #pragma unroll
@@ -245,6 +250,8 @@ __global__ void __launch_bounds__(SpTraits<M>::THREADS, SpTraits<M>::MINB)
                     }
                 }
             }
+        }
+        if (FUSED) {
             acc = block_tree_first<M, TILE_THREADS>(acc, smem);
             if (threadIdx.x == 0) store<W>(part, g.part_ld, g.tile_off + tile, acc);
         }
