@@ -187,7 +187,7 @@ struct SpTraits {
 #ifdef MWCG_SP_U_OVERRIDE
     static constexpr int U = MWCG_SP_U_OVERRIDE;
 #else
-    static constexpr int U = (M == FP64) ? 8 : 4;
+    static constexpr int U = (M == FP64) ? 8 : ((M == TW) ? 3 : 4);  // measured per mode (C2)
 #endif
 };
 
@@ -472,6 +472,11 @@ struct UpTma {
     static constexpr int NS = 2;
 #endif
     static constexpr size_t SMEM = sizeof(double) * STAGE * NS;
+#ifdef MWCG_UP_TMA_MINB
+    static constexpr int MINB = MWCG_UP_TMA_MINB;
+#else
+    static constexpr int MINB = 1;
+#endif
 };
 template <int M>
 struct XpTma {
@@ -510,7 +515,7 @@ __device__ __forceinline__ void tile_issue(double *stage, uint64_t *bar, const d
 }
 
 template <int M, bool FUSED>
-__global__ void __launch_bounds__(TILE_THREADS, 1)
+__global__ void __launch_bounds__(TILE_THREADS, UpTma<M>::MINB)
     cg_update_tma(double *__restrict__ r, const double *__restrict__ q, Geo g, double *__restrict__ part,
                   CgState *st, cudaGraphConditionalHandle h, int use_cond) {
     using Ar = Arith<M>;

@@ -392,3 +392,69 @@ def test_int16_delta_and_int32_columns_agree(mode):
     assert K.device_matrix(far).col_bytes() == 4
     xf = rng.standard_normal((orc.WORDS[mode], far.n_rows))
     assert same_bits(K.spmv(far, _vec(mode, xf)).planes.cpu().numpy(), orc.spmv(mode, far, xf))
+
+
+def _banded_with_holes(n, half, seed, drop):
+    """Banded SPD-ish matrix whose rows miss random off-diagonal entries
+    (slices mix several offset patterns), including rows with only the
+    diagonal and a partial last slice."""
+    rng = np.random.default_rng(seed)
+    rows, cols, vals = [], [], []
+    for i in range(n):
+        for o in range(-half, half + 1):
+            j = i + o
+            if 0 <= j < n and (o == 0 or rng.random() > drop):
+                rows.append(i)
+                cols.append(j)
+                vals.append(4.0 * half if o == 0 else rng.uniform(-1.0, 0.0))
+    order = np.lexsort((cols, rows))
+    r, c, v = np.array(rows)[order], np.array(cols)[order], np.array(vals)[order]
+    rp = np.zeros(n + 1, dtype=np.int64)
+    np.add.at(rp, r + 1, 1)
+    return CsrMatrix(n, n, np.cumsum(rp), c.astype(np.int64), v)
+
+
+@pytest.mark.parametrize("mode", orc.MODES)
+def test_slice_shared_offsets_edge_cases(mode):
+    """Slice-shared offsets (forced) on slices that mix offset patterns,
+    rows holding only the diagonal and a partial last slice: SpMV bitwise
+    equal to the oracle and to the int32 SELL layout."""
+    A = _banded_with_holes(1000 + 13, 3, seed=5, drop=0.35)
+    Ad = CsrMatrix(A.n_rows, A.n_cols, A.row_ptr, A.col_idx, A.values)
+    As = CsrMatrix(A.n_rows, A.n_cols, A.row_ptr, A.col_idx, A.values)
+    assert K.device_matrix(Ad, col_format=2).col_bytes() == 0
+    assert K.device_matrix(As, col_format=0).col_bytes() == 4
+    rng = np.random.default_rng(12)
+    x = rng.standard_normal((orc.WORDS[mode], A.n_rows))
+    yd = K.spmv(Ad, _vec(mode, x)).planes.cpu().numpy()
+    ys = K.spmv(As, _vec(mode, x)).planes.cpu().numpy()
+    assert same_bits(yd, orc.spmv(mode, A, x)) and same_bits(yd, ys)
+
+
+@pytest.mark.parametrize("mode", ["dw", "qtw"])
+def test_slice_shared_offsets_solve_equals_sell(mode):
+    """A whole CG solve gives the same bits in the slice-shared-offset and
+    the SELL layouts."""
+    A = _banded_with_holes(3000, 4, seed=7, drop=0.2)
+    b = problems.spmv_fp64_host(A, np.ones(A.n_rows))
+    conf = cg.SolverConfig(mode=mode, epsilon=1e-20, history_stride=50)
+    got = []
+    for fmt in (2, 1):
+        Af = CsrMatrix(A.n_rows, A.n_cols, A.row_ptr, A.col_idx, A.values)
+        K.device_matrix(Af, col_format=fmt)
+        got.append(cg.cg_solve(Af, b, conf, x_star=np.ones(A.n_rows)))
+    assert got[0].iterations == got[1].iterations and got[0].reason == got[1].reason
+    assert same_bits(got[0].x.planes.cpu().numpy(), got[1].x.planes.cpu().numpy())
+    assert [(h.iteration, h.recurrence_residual) for h in got[0].history] == \
+        [(h.iteration, h.recurrence_residual) for h in got[1].history]
+
+
+def test_slice_shared_offsets_rejected_and_forced_error():
+    """Random columns: the automatic choice falls back to SELL; forcing the
+    slice-shared layout is a ValueError (too many distinct offsets)."""
+    far = random_symmetric(4000, extra_per_row=6, seed=9)
+    assert K.device_matrix(CsrMatrix(far.n_rows, far.n_cols, far.row_ptr, far.col_idx,
+                                     far.values)).col_bytes() in (2, 4)
+    with pytest.raises(ValueError):
+        K.device_matrix(CsrMatrix(far.n_rows, far.n_cols, far.row_ptr, far.col_idx, far.values),
+                        col_format=2)
