@@ -865,6 +865,7 @@ struct mwcg_solver {
     bool dist = false;                   // rank of a row partition (no graph; see dist.py)
     bool tma = false;                    // TMA-staged K3 (aligned planes; MWCG_TMA=0/1 overrides)
     bool tma2 = false;                   // TMA-staged K2 (MWCG_TMA2=0/1 overrides)
+    cudaAccessPolicyWindow l2win{};      // K1's persisting-L2 window over p (num_bytes 0: none)
 };
 
 namespace {
@@ -876,9 +877,21 @@ template <int M, bool FUSED>
 void launch_k1(mwcg_solver *s, cudaStream_t st, cudaGraphConditionalHandle h, int use_cond) {
     const Geo &g = s->geo;
     const unsigned g0 = s->grid[0];
-#define K1_LAUNCH(CT)                                                                                \
-    cg_spmv_pq<M, FUSED, CT><<<g0, SpTraits<M>::THREADS, 0, st>>>(s->A, s->p, s->q, g, s->part, s->st, h, \
-                                                                  use_cond)
+    // K1 carries an L2 access-policy window over p (the gathered vector):
+    // a share of p's lines persists in L2 against the matrix stream and the
+    // random gathers of irregular matrices (C5: p is twice the L2)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(g0);
+    cfg.blockDim = dim3(SpTraits<M>::THREADS);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeAccessPolicyWindow;
+    at[0].val.accessPolicyWindow = s->l2win;
+    cfg.attrs = at;
+    cfg.numAttrs = s->l2win.num_bytes > 0 ? 1 : 0;
+    const double *pc = s->p;
+#define K1_LAUNCH(CT) \
+    cudaLaunchKernelEx(&cfg, cg_spmv_pq<M, FUSED, CT>, s->A, pc, s->q, g, s->part, s->st, h, use_cond)
     if (s->A.dia) K1_LAUNCH(DiaTag);
     else if (s->A.col16) K1_LAUNCH(int16_t);
     else K1_LAUNCH(int32_t);
@@ -992,6 +1005,41 @@ int compute_grids_t(mwcg_solver *s) {
     int dev = 0, sms = 0;
     MWCG_CUDA(cudaGetDevice(&dev));
     MWCG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    {
+        // persisting-L2 window over p for K1: a 32-MB set-aside (measured on
+        // C2: DW 99.4 -> 94.1 us/it, QDW 92.5 -> 87.8, QTW 148.2 -> 140.9; the
+        // persisting lines of p also serve K3's read of p; larger set-asides
+        // starve the other vectors: 64 MB -> DW 139 us/it; neutral for FP64,
+        // C4 and C5).  MWCG_L2PIN=0 disables, =<MB> sets the set-aside.
+        const char *t = std::getenv("MWCG_L2PIN");
+        int max_persist = 0, max_win = 0;
+        cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
+        cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+        const size_t pbytes = sizeof(double) * (size_t)Arith<M>::W * (size_t)s->geo.ldp;
+        size_t aside = std::min((size_t)max_persist, (size_t)32 << 20);
+        if (t && atoi(t) > 0) aside = std::min((size_t)max_persist, (size_t)atoi(t) << 20);
+        const bool on = t ? t[0] != '0' : (Arith<M>::W >= 2);
+        s->l2win = cudaAccessPolicyWindow{};
+        if (on && aside > 0 && max_win > 0 && pbytes > 0) {
+            // the device-wide set-aside is configured once per process and size
+            // (re-setting it per solver reconfigures the L2: seen as a 2x slower
+            // create-solve-destroy loop)
+            static size_t configured = 0;
+            if (configured != aside) {
+                cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, aside);
+                configured = aside;
+            }
+            size_t cur = 0;
+            cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+            const size_t win = std::min(pbytes, (size_t)max_win);
+            s->l2win.base_ptr = s->p;
+            s->l2win.num_bytes = win;
+            s->l2win.hitRatio = (float)std::min(1.0, (double)cur / (double)win);
+            s->l2win.hitProp = cudaAccessPropertyPersisting;
+            s->l2win.missProp = cudaAccessPropertyStreaming;
+        }
+        cudaGetLastError();  // the limit calls are advisory
+    }
     int nb[4] = {1, 1, 1, 1};
     {
         // TMA-staged vector passes: measured faster for QTW (C2: K2 62.6 ->

@@ -19,8 +19,10 @@ torch.cuda.synchronize()
 print(f"sell {time.time()-t:.1f}s padded={dm.padded_entries()} ({dm.padded_entries()/A.nnz:.3f}x) "
       f"col_bytes={dm.col_bytes()}", flush=True)
 for mode in sys.argv[2].split(",") if len(sys.argv) > 2 else ("dw", "qtw"):
-    conf = cg.SolverConfig(mode=mode, epsilon=c["epsilon"], max_iterations=c["max_iterations"],
-                           history_stride=10**9)
+    kern = os.environ.get("C5_KERNELS") == "1"  # kernel-by-kernel launches (for ncu)
+    conf = cg.SolverConfig(mode=mode, epsilon=c["epsilon"] if not kern else 1e-300,
+                           max_iterations=c["max_iterations"] if not kern else 6,
+                           history_stride=10**9, timing="kernels" if kern else "graph")
     r = cg.cg_solve(A, c["b"], conf)
     r = cg.cg_solve(A, c["b"], conf)
     B = 12 * A.nnz + 4 * (A.n_rows + 1) + 72 * {"fp64": 1, "dw": 2, "qdw": 2, "tw": 3, "qtw": 3}[mode] * A.n_rows
