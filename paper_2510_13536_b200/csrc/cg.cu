@@ -911,11 +911,14 @@ void launch_k2(mwcg_solver *s, cudaStream_t st, cudaGraphConditionalHandle h, in
 
 template <int M>
 void launch_k3(mwcg_solver *s, cudaStream_t st, cudaGraphConditionalHandle h, int use_cond) {
-    if (s->tma)
-        cg_xpay_tma<M><<<s->grid[2], TILE_THREADS, XpTma<M>::SMEM, st>>>(s->x, s->p, s->r, s->geo, s->st, h,
-                                                                         use_cond);
-    else
-        cg_xpay<M><<<s->grid[2], TILE_THREADS, 0, st>>>(s->x, s->p, s->r, s->geo, s->st, h, use_cond);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(s->grid[2]);
+    cfg.blockDim = dim3(TILE_THREADS);
+    cfg.dynamicSmemBytes = s->tma ? XpTma<M>::SMEM : 0;
+    cfg.stream = st;
+    const double *rc = s->r;
+    if (s->tma) cudaLaunchKernelEx(&cfg, cg_xpay_tma<M>, s->x, s->p, rc, s->geo, s->st, h, use_cond);
+    else cudaLaunchKernelEx(&cfg, cg_xpay<M>, s->x, s->p, rc, s->geo, s->st, h, use_cond);
 }
 
 // stage 0: K1 [+ reference p.q], 1: K2 [+ reference r.r], 2: K3
@@ -1656,6 +1659,12 @@ int mwcg_cg_solve(mwcg_solver *s, const double *b, double b_norm, const double *
     if (history_stride < 1) {
         set_error("history_stride must be >= 1");
         return MWCG_ERR_VALUE;
+    }
+    if (s->l2win.num_bytes > 0) {
+        // persisting lines left by earlier solvers (other p buffers, possibly
+        // freed) would hold the set-aside: return them to normal first
+        MWCG_CUDA(cudaStreamSynchronize(s->stream));
+        cudaCtxResetPersistingL2Cache();
     }
     int rc = mwcg_solver_start(s, b, b_norm, x0, x_star, epsilon, max_iterations);
     if (rc) return rc;

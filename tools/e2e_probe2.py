@@ -25,7 +25,7 @@ cg.device_matrix = kernels.device_matrix
 cg.Solver.__init__ = timed("solver_init", cg.Solver.__init__)
 cg.Solver.solve = timed("solver_solve", cg.Solver.solve)
 cg._b_norm = timed("b_norm", cg._b_norm)
-for it in range(5):
+for it in range(int(os.environ.get("E2E_STEPS", "5"))):
     T.clear()
     Ah = CsrMatrix.__new__(CsrMatrix)
     for k, v in (("n_rows", n), ("n_cols", n), ("row_ptr", pin["rp"].numpy()), ("col_idx", pin["ci"].numpy()),
