@@ -436,14 +436,19 @@ def run_ours(a):
         barrier()
         t0 = time.perf_counter()
         e_it = 0
+        step_ms = []
         for _ in range(a.steps):
+            ts = time.perf_counter()
             r, _ = e2e_step()
             e_it += int(r.iterations)
+            step_ms.append(1e3 * (time.perf_counter() - ts))
         barrier()
         e_dt = max_over_ranks(time.perf_counter() - t0)
+        print("e2e step ms: " + " ".join(f"{v:.1f}" for v in step_ms), file=sys.stderr, flush=True)
         e2e = {"value": sum_over_ranks(e_it) / e_dt, "unit": "iter/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "ms_per_step": 1e3 * e_dt / a.steps,
+               "ms_per_step_median": statistics.median(step_ms),
                "path": "cg_solve(CsrMatrix(host, pinned), b host) -> x words to host"}
 
     # ---- CPU baseline (rank 0, N=1 only) -------------------------------------
