@@ -148,6 +148,9 @@ int mwcg_solver_start(mwcg_solver *s, const double *b, double b_norm, const doub
 int mwcg_solver_run(mwcg_solver *s, int64_t k_stop);
 /* same, kernel-by-kernel with CUDA events; ms[0..2] += per-stage device ms */
 int mwcg_solver_run_profiled(mwcg_solver *s, int64_t k_stop, double *ms);
+/* Device µs of one SpMV+p.q launch (K1), averaged over `reps` back-to-back
+ * launches on a started solver (bench.py's roofline.launch_us). */
+int mwcg_solver_time_k1(mwcg_solver *s, int reps, double *us);
 int mwcg_solver_state(mwcg_solver *s, mwcg_state *out);
 /* norm_metrics_tw (kernels.py:305-328) of the current iterate */
 int mwcg_solver_metrics(mwcg_solver *s, double *err, double *true_res);

@@ -74,6 +74,7 @@ SIGNATURES = {
     "mwcg_solver_start": (ctypes.c_int, [c_vp, c_vp, ctypes.c_double, c_vp, c_vp,
                                          ctypes.c_double, c_i64]),
     "mwcg_solver_run": (ctypes.c_int, [c_vp, c_i64]),
+    "mwcg_solver_time_k1": (ctypes.c_int, [c_vp, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]),
     "mwcg_solver_run_profiled": (ctypes.c_int, [c_vp, c_i64, c_dp]),
     "mwcg_solver_state": (ctypes.c_int, [c_vp, ctypes.POINTER(StateC)]),
     "mwcg_solver_metrics": (ctypes.c_int, [c_vp, c_dp, c_dp]),

@@ -154,6 +154,17 @@ def _host_pool():
     return _POOL
 
 
+def _time_k1(solver, b_dev, b_norm, reps=20):
+    """Device µs of one K1 launch (SpMV + p.q + alpha) on a freshly started
+    solve: `reps` back-to-back launches between CUDA events."""
+    L = solver._L
+    _lib.check(L.mwcg_solver_start(solver.handle, _lib.ptr(b_dev), float(b_norm), None, None,
+                                   1e-300, 10**9))
+    us = ctypes.c_double()
+    _lib.check(L.mwcg_solver_time_k1(solver.handle, int(reps), ctypes.byref(us)))
+    return us.value
+
+
 def _b_norm(b):
     out = ctypes.c_double()
     _lib.check(_lib.load().mwcg_norm2_host(b.ctypes.data_as(_lib.c_dp), b.size, ctypes.byref(out)))

@@ -823,61 +823,6 @@ __global__ void __launch_bounds__(TILE_THREADS)
     }
 }
 
-// Fused history metrics (tile order): one tile per CTA computes the TW
-// residual rows b - A x and the error rows x* - x and accumulates their TW
-// squares -- and, on a solve's first record, those of b and x* -- in the
-// canonical tile order, then the last CTA reduces the tile partials.  Bitwise
-// the metrics_vec_kernel + dot_tile_kernel<TW> sequence (same row values,
-// same per-thread order, same trees) without the res/diff round trip through
-// HBM and with 1 launch instead of 3-5.  out: res, diff, b, x* (3 words each).
-template <typename CT>
-__global__ void __launch_bounds__(TILE_THREADS)
-    metrics_tile_kernel(SellMatrix A, const double *__restrict__ xt, const double *__restrict__ b,
-                        const double *__restrict__ xs, int first, double *__restrict__ part, int64_t ntiles,
-                        unsigned int *ticket, double *__restrict__ out) {
-    __shared__ double smem[3 * TILE_THREADS / 32];
-    __shared__ int s_last;
-    const int64_t n = A.n_rows;
-    const int64_t base = (int64_t)blockIdx.x * TILE + threadIdx.x;
-    V<3> acc[4] = {zero<3>(), zero<3>(), zero<3>(), zero<3>()};
-#pragma unroll 1
-    for (int j = 0; j < TILE_ELEMS; j++) {
-        const int64_t i = base + j * TILE_THREADS;
-        if (i < n) {
-            const V<3> qi = spmv_row<TW, 8, CT>(A, xt, n, i);
-            const V<3> ri = dxtw_add(b[i], neg<3>(qi));
-            acc[0] = tw_add(acc[0], tw_mul(ri, ri));
-            if (xs) {
-                const V<3> di = dxtw_add(xs[i], neg<3>(load<3>(xt, n, i)));
-                acc[1] = tw_add(acc[1], tw_mul(di, di));
-            }
-            if (first) {
-                const V<3> bi{{b[i], 0.0, 0.0}};
-                acc[2] = tw_add(acc[2], tw_mul(bi, bi));
-                if (xs) {
-                    const V<3> xi{{xs[i], 0.0, 0.0}};
-                    acc[3] = tw_add(acc[3], tw_mul(xi, xi));
-                }
-            }
-        }
-    }
-    const int nq = first ? 4 : 2;
-#pragma unroll 1
-    for (int k = 0; k < nq; k++) {
-        const V<3> r = block_tree<TW, TILE_THREADS>(acc[k], smem);
-        if (threadIdx.x == 0) store<3>(part + 3 * ntiles * k, ntiles, blockIdx.x, r);
-    }
-    if (!last_block_done(ticket, &s_last)) return;
-#pragma unroll 1
-    for (int k = 0; k < nq; k++) {
-        const V<3> r = reduce_partials_block<TW>(part + 3 * ntiles * k, ntiles, ntiles, smem);
-        if (threadIdx.x == 0)
-#pragma unroll
-            for (int w = 0; w < 3; w++) out[3 * k + w] = r.w[w];
-    }
-    if (threadIdx.x == 0) *ticket = 0u;
-}
-
 }  // namespace mwcg
 
 // =====================================================================
@@ -1570,6 +1515,47 @@ int mwcg_solver_run(mwcg_solver *s, int64_t k_stop) {
     return 0;
 }
 
+// Device duration of the SpMV kernel (K1) alone: `reps` back-to-back
+// launches between two events on the solver's stream (no host gaps).  K1 is
+// idempotent on a running state (q = A p, the p.q partials and alpha are
+// recomputed from the same p and rho), so this is valid after
+// mwcg_solver_start; the state's pause point is lifted for the measurement.
+int mwcg_solver_time_k1(mwcg_solver *s, int reps, double *us) {
+    if (!s || !us || reps < 1) {
+        set_error("bad argument");
+        return MWCG_ERR_VALUE;
+    }
+    if (s->n == 0) {
+        *us = 0.0;
+        return 0;
+    }
+    cudaStream_t st = s->stream;
+    MWCG_CUDA(cudaStreamSynchronize(st));
+    *s->kstop_host = LLONG_MAX;
+    MWCG_CUDA(cudaMemcpyAsync(&s->st->k_stop, s->kstop_host, sizeof(long long), cudaMemcpyHostToDevice, st));
+    MWCG_CUDA(cudaMemsetAsync(&s->st->pause, 0, sizeof(int), st));
+    cudaGraphConditionalHandle h{};
+    for (int pass = 0; pass < 2; pass++) {  // pass 0 warms up
+        MWCG_CUDA(cudaEventRecord(s->ev[6], st));
+        for (int r = 0; r < reps; r++) {
+            switch (s->mode) {
+            case FP64: s->fused ? launch_k1<FP64, true>(s, st, h, 0) : launch_k1<FP64, false>(s, st, h, 0); break;
+            case DW: s->fused ? launch_k1<DW, true>(s, st, h, 0) : launch_k1<DW, false>(s, st, h, 0); break;
+            case QDW: s->fused ? launch_k1<QDW, true>(s, st, h, 0) : launch_k1<QDW, false>(s, st, h, 0); break;
+            case TW: s->fused ? launch_k1<TW, true>(s, st, h, 0) : launch_k1<TW, false>(s, st, h, 0); break;
+            default: s->fused ? launch_k1<QTW, true>(s, st, h, 0) : launch_k1<QTW, false>(s, st, h, 0); break;
+            }
+        }
+        MWCG_CHECK_LAUNCH();
+        MWCG_CUDA(cudaEventRecord(s->ev[7], st));
+        MWCG_CUDA(cudaEventSynchronize(s->ev[7]));
+    }
+    float ms = 0.f;
+    MWCG_CUDA(cudaEventElapsedTime(&ms, s->ev[6], s->ev[7]));
+    *us = 1e3 * (double)ms / reps;
+    return 0;
+}
+
 // Same as run, but one kernel launch at a time with CUDA events around each
 // stage; accumulates device milliseconds into ms[0..2] = K1, K2, K3 (fused)
 // or K1, K2, K3 incl. the reference dots (partitions mode).
@@ -1655,32 +1641,13 @@ int mwcg_solver_metrics(mwcg_solver *s, double *err, double *true_res) {
         MWCG_CUDA(pool_alloc((void **)&s->res, b3, st));
         MWCG_CUDA(pool_alloc((void **)&s->diff, b3, st));
         MWCG_CUDA(pool_alloc((void **)&s->bt, b3, st));
-        MWCG_CUDA(pool_alloc((void **)&s->mpart, sizeof(double) * 12 * (size_t)(s->ntiles > 0 ? s->ntiles : 1), st));
+        MWCG_CUDA(pool_alloc((void **)&s->mpart, sizeof(double) * 3 * (size_t)(s->ntiles > 0 ? s->ntiles : 1), st));
         MWCG_CUDA(pool_alloc((void **)&s->mout, sizeof(double) * 12, st));
         MWCG_CUDA(pool_alloc((void **)&s->mticket, sizeof(unsigned int), st));
         MWCG_CUDA(cudaMemsetAsync(s->mticket, 0, sizeof(unsigned int), st));
     }
     const unsigned eb = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16);
     int rc;
-    if (s->fused) {  // tile order: one fused kernel (metrics_tile_kernel)
-        switch (s->mode) {
-        case FP64: promote_kernel<FP64><<<eb, 256, 0, st>>>(n, s->x, n, s->xt); break;
-        case DW: promote_kernel<DW><<<eb, 256, 0, st>>>(n, s->x, n, s->xt); break;
-        case QDW: promote_kernel<QDW><<<eb, 256, 0, st>>>(n, s->x, n, s->xt); break;
-        case TW: promote_kernel<TW><<<eb, 256, 0, st>>>(n, s->x, n, s->xt); break;
-        default: promote_kernel<QTW><<<eb, 256, 0, st>>>(n, s->x, n, s->xt); break;
-        }
-        const int first = s->norms_ready ? 0 : 1;
-        const unsigned nt = (unsigned)s->ntiles;
-#define MT(CT)                                                                                         \
-    metrics_tile_kernel<CT><<<nt, TILE_THREADS, 0, st>>>(s->A, s->xt, s->b, s->x_star, first, s->mpart,  \
-                                                         s->ntiles, s->mticket, s->mout)
-        if (s->A.dia) MT(DiaTag);
-        else if (s->A.col16) MT(int16_t);
-        else MT(int32_t);
-#undef MT
-        MWCG_CHECK_LAUNCH();
-    } else {
     if (!s->norms_ready) {
         promote_fp64_kernel<<<eb, 256, 0, st>>>(n, s->b, s->bt);
         if ((rc = tw_sumsq(s, s->bt, 2))) return rc;
@@ -1705,7 +1672,6 @@ int mwcg_solver_metrics(mwcg_solver *s, double *err, double *true_res) {
     MWCG_CHECK_LAUNCH();
     if ((rc = tw_sumsq(s, s->res, 0))) return rc;
     if (s->x_star && (rc = tw_sumsq(s, s->diff, 1))) return rc;
-    }
     MWCG_CUDA(cudaMemcpyAsync(s->mout_host, s->mout, sizeof(double) * 12, cudaMemcpyDeviceToHost, st));
     MWCG_CUDA(cudaStreamSynchronize(st));
     auto coll = [](const double *v) { return (v[0] + v[1]) + v[2]; };
@@ -1756,13 +1722,10 @@ int mwcg_cg_solve(mwcg_solver *s, const double *b, double b_norm, const double *
         const bool first = !s->norms_ready;
         int r2 = mwcg_solver_metrics(s, &e, &t);
         if (r2) return r2;
-        if (s->fused) {
-            metric_launches += 2;  // promote x + metrics_tile_kernel
-        } else {
-            // promote x, metrics rows, 1-2 dots of 2 kernels each (partitions mode)
-            metric_launches += 2 + 2 * (s->x_star ? 2 : 1);
-            if (first) metric_launches += 3 * (s->x_star ? 2 : 1);
-        }
+        // promote x, metrics rows, 1-2 dots (2 kernels each in partitions mode)
+        const int dk = s->fused ? 1 : 2;
+        metric_launches += 2 + dk * (s->x_star ? 2 : 1);
+        if (first) metric_launches += (1 + dk) * (s->x_star ? 2 : 1);
         cudaEventRecord(s->ev[5], s->stream);
         cudaEventSynchronize(s->ev[5]);
         float ms = 0;

@@ -55,11 +55,4 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     }
 }
 
-// bulk L2 prefetch of a contiguous global range (bytes: multiple of 16,
-// 16-B aligned): the copy engine pulls it into L2 with no register or shared
-// memory cost
-__device__ __forceinline__ void prefetch_l2(const void *src, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
-}
-
 }  // namespace mwcg
