@@ -105,7 +105,9 @@ class Solver:
     def __init__(self, A, mode, normalization="after-axpy", reduction="tile", partitions=1):
         if isinstance(normalization, Normalization):
             normalization = normalization.value
-        self.A = A
+        # no reference back to A: A caches its solvers (A._solvers), and a
+        # cycle A -> solver -> A would leave every matrix/solver pair to the
+        # cyclic GC (freed in bursts, the device pool growing meanwhile)
         self.mode = mode
         self.w = mode_words(mode)
         self.n = A.n_rows
