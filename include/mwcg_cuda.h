@@ -181,6 +181,24 @@ int mwcg_solver_create_dist(mwcg_solver **out, const mwcg_matrix *A, const mwcg_
 /* stream: NULL = the solver's stream (graph capture passes the capture stream) */
 int mwcg_solver_dist_stage(mwcg_solver *s, int stage, void *stream);
 
+/* ---- ingestion: Matrix Market coordinate text (sparse.py:115-196) ----
+ * Two calls: with rows == NULL it parses the banner and size line into info;
+ * then with rows/cols/vals of info->nnz entries it parses the entries (0-based
+ * indices, file order; the caller builds the CSR, summing duplicates).
+ * Returns 0, MWCG_MM_ERROR (malformed input: mwcg_last_error() holds the
+ * reference's message, info->error_line its line number, -1 if none), or
+ * MWCG_MM_FALLBACK (input outside the native grammar -- non-ASCII bytes, lone
+ * CR, '_' separators, hex floats, int64 overflow -- parse it the Python way). */
+enum { MWCG_MM_ERROR = 1101, MWCG_MM_FALLBACK = 1102 };
+typedef struct {
+    int64_t n_rows, n_cols, nnz;
+    int symmetric;
+    int reserved;
+    int64_t error_line;
+} mwcg_mm_info;
+int mwcg_mm_parse(const char *data, int64_t len, mwcg_mm_info *info, int64_t *rows, int64_t *cols,
+                  double *vals);
+
 /* ---- measurement helpers (bench.py) ---- */
 /* FP64 pipe microbenchmark: DFMA chains on all SMs; returns FP64 ops/s
  * (FMA = 1 op, the SURVEY §8(d) convention) and the elapsed ms. */

@@ -37,6 +37,15 @@ class StateC(ctypes.Structure):
                 ("beta", ctypes.c_double * 3)]
 
 
+class MmInfoC(ctypes.Structure):
+    _fields_ = [("n_rows", c_i64), ("n_cols", c_i64), ("nnz", c_i64), ("symmetric", ctypes.c_int),
+                ("reserved", ctypes.c_int), ("error_line", c_i64)]
+
+
+MM_ERROR = 1101
+MM_FALLBACK = 1102
+
+
 class SolveResultC(ctypes.Structure):
     _fields_ = [("iterations", c_i64), ("n_hist", c_i64), ("status", ctypes.c_int),
                 ("reserved", ctypes.c_int), ("final_rel", ctypes.c_double),
@@ -74,6 +83,7 @@ SIGNATURES = {
     "mwcg_solver_start": (ctypes.c_int, [c_vp, c_vp, ctypes.c_double, c_vp, c_vp,
                                          ctypes.c_double, c_i64]),
     "mwcg_solver_run": (ctypes.c_int, [c_vp, c_i64]),
+    "mwcg_mm_parse": (ctypes.c_int, [ctypes.c_char_p, c_i64, ctypes.POINTER(MmInfoC), c_vp, c_vp, c_vp]),
     "mwcg_solver_time_k1": (ctypes.c_int, [c_vp, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]),
     "mwcg_solver_run_profiled": (ctypes.c_int, [c_vp, c_i64, c_dp]),
     "mwcg_solver_state": (ctypes.c_int, [c_vp, ctypes.POINTER(StateC)]),
