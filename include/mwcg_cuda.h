@@ -199,6 +199,19 @@ typedef struct {
 int mwcg_mm_parse(const char *data, int64_t len, mwcg_mm_info *info, int64_t *rows, int64_t *cols,
                   double *vals);
 
+/* ---- exact problem generation (problemgen.py:47-108, `generate`) ----
+ * Replaces the reference's pure-Python ExactValue row sums (oracle.py:35-128)
+ * for the all-ones solution: b_i = the exact row sum rounded to nearest FP64,
+ * the rounding gap absorbed into the diagonal, b_i nudged by up to 4 ulps until
+ * the perturbed diagonal is an FP64 number (problemgen.py:37-44).  Host code;
+ * `threads` host threads over rows (<= 0: all).  CSR is int64, columns sorted
+ * inside each row.  new_values (nnz) may alias values; b and deltas have n
+ * entries (deltas[i] = FP64 new_diag - old_diag, 0 where unchanged).  Returns
+ * 0 or MWCG_ERR_VALUE with the reference's message for the first failing row. */
+int mwcg_problem_generate(int64_t n, const int64_t *row_ptr, const int64_t *col_idx,
+                          const double *values, double *new_values, double *b, double *deltas,
+                          int64_t *max_ulp_adjustment, int threads);
+
 /* ---- measurement helpers (bench.py) ---- */
 /* FP64 pipe microbenchmark: DFMA chains on all SMs; returns FP64 ops/s
  * (FMA = 1 op, the SURVEY §8(d) convention) and the elapsed ms. */

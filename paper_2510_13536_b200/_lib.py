@@ -84,6 +84,8 @@ SIGNATURES = {
                                          ctypes.c_double, c_i64]),
     "mwcg_solver_run": (ctypes.c_int, [c_vp, c_i64]),
     "mwcg_mm_parse": (ctypes.c_int, [ctypes.c_char_p, c_i64, ctypes.POINTER(MmInfoC), c_vp, c_vp, c_vp]),
+    "mwcg_problem_generate": (ctypes.c_int, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                             ctypes.POINTER(c_i64), ctypes.c_int]),
     "mwcg_solver_time_k1": (ctypes.c_int, [c_vp, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]),
     "mwcg_solver_run_profiled": (ctypes.c_int, [c_vp, c_i64, c_dp]),
     "mwcg_solver_state": (ctypes.c_int, [c_vp, ctypes.POINTER(StateC)]),

@@ -16,7 +16,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libmwcg_cuda.so")
-SOURCES = ["capi.cu", "sell.cu", "ops.cu", "cg.cu", "mm.cu"]
+SOURCES = ["capi.cu", "sell.cu", "ops.cu", "cg.cu", "mm.cu", "problemgen.cu"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
