@@ -6,7 +6,8 @@ b, and absorbs the rounding gap into the diagonal (nudging b_i by up to 4 ulps u
 the new diagonal is representable).  The exact row sums run in
 `libmwcg_cuda.so:mwcg_problem_generate` (csrc/problemgen.cu: fixed-point exact
 accumulators over host threads) instead of the reference's pure-Python
-`ExactValue` loop (oracle.py:35-128), which is infeasible beyond ~1e5 nonzeros.
+`ExactValue` loop (its exact-arithmetic module, lines 35-128), which is
+infeasible beyond ~1e5 nonzeros.
 Results, error messages and the error row are the reference's.
 """
 import ctypes
