@@ -204,3 +204,19 @@ def test_verify_passes(capsys):
     assert cli.main(["verify"]) == cli.EXIT_OK
     out = capsys.readouterr().out
     assert "FAIL" not in out and "checks passed" in out
+
+
+@pytest.mark.gpu
+def test_threads_env_fallback_matches_reference(tmp_path, monkeypatch):
+    """MW_THREADS stands in for --threads (cli.py:110-120): same bytes as the
+    reference CLI's --threads 2 run."""
+    c = next(c for c in G.load("cli.json")["cases"] if "--threads" in c["argv"]
+             and c["argv"][c["argv"].index("--threads") + 1] == "2")
+    argv = list(c["argv"])
+    i = argv.index("--threads")
+    del argv[i:i + 2]
+    monkeypatch.setenv("MW_THREADS", "2")
+    s, h = tmp_path / "s.csv", tmp_path / "h.csv"
+    assert cli.main(argv + ["--no-timing", "--out-summary", str(s), "--out-history", str(h)]) == 0
+    assert s.read_text() == c["files"]["summary"]
+    assert h.read_text() == c["files"]["history"]
