@@ -103,6 +103,16 @@ def test_generate_output_parses_back(tmp_path):
     assert np.array([float(v) for v in lines[2:]]).size == 30
 
 
+def test_solve_without_gpu_fails_loudly():
+    """No CPU fallback: without a device the solve raises instead of computing."""
+    import torch
+    from paper_2510_13536_b200._lib import MwcgError
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    with pytest.raises(MwcgError, match="no CPU fallback"):
+        cli.main(["solve", "--synthetic", "identity:4"])
+
+
 # ---- device runs ----
 
 @pytest.mark.gpu
