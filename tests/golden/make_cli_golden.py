@@ -30,14 +30,36 @@ SOLVE = [
     ["solve", "--synthetic", "laplacian2d:6", "--mode", "qdw", "--threads", "4",
      "--max-iters", "5", "--eps", "1e-30", "--stride", "2"],
 ]
+# a symmetric Matrix Market input (lower triangle of a scaled Laplacian); the
+# path is relative to the repo root because it is the `matrix` label in the outputs
+MTX = os.path.join("tests", "golden", "cli_sym.mtx")
+SOLVE += [
+    ["solve", "--matrix", MTX, "--mode", "qtw", "--mode", "dw", "--eps", "1e-26", "--threads", "2",
+     "--normalize", "every-op", "--stride", "4", "--reps", "2"],
+    ["solve", "--matrix", MTX, "--mode", "tw", "--mode", "fp64", "--eps", "1e-14", "--threads", "5",
+     "--normalize", "none"],
+]
 GENERATE = [
     ["generate", "--synthetic", "random:30:7"],
     ["generate", "--synthetic", "scaled-laplacian2d:5:3:8"],
 ]
 
 
+def _write_fixture(sparse):
+    A = sparse.scaled_laplacian_2d(7, 4.0, 5)
+    ents = [(i, int(A.col_idx[k]), float(A.values[k])) for i in range(A.n_rows)
+            for k in range(A.row_ptr[i], A.row_ptr[i + 1]) if A.col_idx[k] <= i]
+    with open(os.path.join(HERE, "..", "..", MTX), "w") as f:
+        f.write("%%MatrixMarket matrix coordinate real symmetric\n")
+        f.write(f"{A.n_rows} {A.n_cols} {len(ents)}\n")
+        for i, j, v in ents:
+            f.write(f"{i + 1} {j + 1} {v!r}\n")
+
+
 def main():
-    _import_reference()
+    _, _, _, _, sparse = _import_reference()
+    _write_fixture(sparse)
+    os.chdir(os.path.join(HERE, "..", ".."))
     from mwcg import cli
     cases = []
     with tempfile.TemporaryDirectory() as d:

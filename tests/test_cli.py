@@ -9,6 +9,7 @@ partition reduction order; generate: host, native problem generator).
 """
 import csv
 import json
+import os
 
 import numpy as np
 import pytest
@@ -116,9 +117,11 @@ def test_solve_without_gpu_fails_loudly():
 # ---- device runs ----
 
 @pytest.mark.gpu
-def test_solve_matches_reference_bytes(tmp_path):
+def test_solve_matches_reference_bytes(tmp_path, monkeypatch):
     """--no-timing + --threads P: the device solve in the reference's P-partition
-    order writes the reference CLI's summary, history and JSON byte for byte."""
+    order writes the reference CLI's summary, history and JSON byte for byte
+    (synthetic inputs and a symmetric Matrix Market file)."""
+    monkeypatch.chdir(os.path.dirname(G.GOLDEN.rstrip("/")) + "/..")
     n = 0
     for c in G.load("cli.json")["cases"]:
         if c["argv"][0] != "solve":
@@ -131,7 +134,7 @@ def test_solve_matches_reference_bytes(tmp_path):
         assert h.read_text() == c["files"]["history"], c["argv"]
         assert j.read_text() == c["files"]["json"], c["argv"]
         n += 1
-    assert n == 6
+    assert n == 8
 
 
 @pytest.mark.gpu
