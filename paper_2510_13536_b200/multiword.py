@@ -8,7 +8,17 @@ from typing import NamedTuple
 
 import numpy as np
 
-__all__ = ["DoubleWord", "TripleWord", "scalar_op", "dw_to_fp64", "tw_to_fp64"]
+__all__ = [
+    "DoubleWord", "TripleWord", "scalar_op",
+    "dw_add", "dw_mul", "dw_neg", "dw_sub", "dw_div",
+    "qdw_add", "qdw_mul", "qdw_div",
+    "tw_add", "tw_mul", "tw_neg", "tw_sub", "tw_div",
+    "qtw_add", "qtw_mul", "qtw_div",
+    "dxdw_add", "dxdw_mul", "dxqdw_add", "dxqdw_mul",
+    "dxtw_add", "dxtw_mul", "dxqtw_add", "dxqtw_mul",
+    "normalize_dw", "normalize_tw",
+    "dw_from_fp64", "tw_from_fp64", "dw_to_fp64", "tw_to_fp64",
+]
 
 
 class DoubleWord(NamedTuple):
@@ -66,3 +76,56 @@ def scalar_op(op, mode, a, b=None):
     _lib.check(L.mwcg_scalar_op(OPS[op], _lib.MODE_ID[mode], _lib.ptr(A), _lib.ptr(B),
                                 _lib.ptr(out), _lib.stream_handle()))
     return out.cpu().numpy()
+
+
+# ---------------------------------------------------------------------------
+# The reference's scalar API (multiword.py:18-409), each op one device launch
+# of the same arithmetic the kernels use (csrc/mw.cuh); results are
+# DoubleWord / TripleWord values.
+# ---------------------------------------------------------------------------
+
+def _run(op, mode, a, b=None):
+    w = 2 if mode in ("dw", "qdw") else 3
+    r = scalar_op(op, mode, a, b)
+    return DoubleWord(float(r[0]), float(r[1])) if w == 2 else TripleWord(*map(float, r[:3]))
+
+
+def dw_from_fp64(x):
+    return DoubleWord(float(x), 0.0)
+
+
+def tw_from_fp64(x):
+    return TripleWord(float(x), 0.0, 0.0)
+
+
+def dw_add(a, b): return _run("add", "dw", a, b)           # noqa: E704
+def dw_mul(a, b): return _run("mul", "dw", a, b)           # noqa: E704
+def dw_neg(a): return _run("neg", "dw", a)                 # noqa: E704
+def dw_sub(a, b): return dw_add(a, dw_neg(b))              # noqa: E704  (multiword.py:135-136)
+def dw_div(a, b): return _run("div", "dw", a, b)           # noqa: E704
+def qdw_add(a, b): return _run("add", "qdw", a, b)         # noqa: E704
+def qdw_mul(a, b): return _run("mul", "qdw", a, b)         # noqa: E704
+def tw_add(a, b): return _run("add", "tw", a, b)           # noqa: E704
+def tw_mul(a, b): return _run("mul", "tw", a, b)           # noqa: E704
+def tw_neg(a): return _run("neg", "tw", a)                 # noqa: E704
+def tw_sub(a, b): return tw_add(a, tw_neg(b))              # noqa: E704  (multiword.py:259-260)
+def tw_div(a, b): return _run("div", "tw", a, b)           # noqa: E704
+def qtw_add(a, b): return _run("add", "qtw", a, b)         # noqa: E704
+def qtw_mul(a, b): return _run("mul", "qtw", a, b)         # noqa: E704
+def dxdw_add(a, b): return _run("dxadd", "dw", [a], b)     # noqa: E704
+def dxdw_mul(a, b): return _run("dxmul", "dw", [a], b)     # noqa: E704
+def dxqdw_add(a, b): return _run("dxadd", "qdw", [a], b)   # noqa: E704
+def dxqdw_mul(a, b): return _run("dxmul", "qdw", [a], b)   # noqa: E704
+def dxtw_add(a, b): return _run("dxadd", "tw", [a], b)     # noqa: E704
+def dxtw_mul(a, b): return _run("dxmul", "tw", [a], b)     # noqa: E704
+def dxqtw_add(a, b): return _run("dxadd", "qtw", [a], b)   # noqa: E704
+def dxqtw_mul(a, b): return _run("dxmul", "qtw", [a], b)   # noqa: E704
+# normalize_dw is the QuickTwoSum/TwoSum renormalisation of the quasi kernels
+# (_fast.py:121-126); normalize_tw the VecSum renormalisation (_fast.py:129-133)
+def normalize_dw(a): return _run("normalize", "qdw", a)    # noqa: E704
+def normalize_tw(a): return _run("normalize", "qtw", a)    # noqa: E704
+
+
+# the quasi modes reuse the normalized divisions (multiword.py:405-409)
+qdw_div = dw_div
+qtw_div = tw_div
