@@ -129,7 +129,8 @@ int mwcg_residual(int mode, int64_t n, const double *b, const double *q, int64_t
 int mwcg_normalize(int mode, int64_t n, double *v, int64_t ld, void *stream);
 /* scalar ops on device pointers (3 doubles each), codes:
  * 0 add 1 mul 2 dxmul 3 dxadd 4 normalize 5 div 6 neg 7 two_sum
- * 8 quick_two_sum 9 two_prod 10 collapse (multiword.py / eft.py) */
+ * 8 quick_two_sum 9 two_prod 10 collapse 11 fma (a[0]*b[0]+a[1], one rounding)
+ * (multiword.py / eft.py) */
 int mwcg_scalar_op(int op, int mode, const double *a, const double *b, double *out, void *stream);
 /* norm2_fp64 (kernels.py:290-296, sumsq_collapsed_1 _fast.py:565-571):
  * sequential unfused sum of squares of a HOST vector, then sqrt. */

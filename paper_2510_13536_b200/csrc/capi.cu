@@ -137,7 +137,7 @@ int mwcg_normalize(int mode, int64_t n, double *v, int64_t ld, void *stream) {
 }
 
 int mwcg_scalar_op(int op, int mode, const double *a, const double *b, double *out, void *stream) {
-    if (!valid_mode(mode) || op < 0 || op > 10) {
+    if (!valid_mode(mode) || op < 0 || op > 11) {
         set_error("bad mode or op");
         return MWCG_ERR_VALUE;
     }

@@ -158,6 +158,7 @@ __global__ void scalar_op_kernel(int op, const double *a, const double *b, doubl
     case 8: quick_two_sum(a[0], b[0], r0, r1); break;
     case 9: two_prod(a[0], b[0], r0, r1); break;
     case 10: R.w[0] = Ar::collapse(A); break;
+    case 11: R.w[0] = __fma_rn(a[0], b[0], a[1]); break;  // eft.fma: c rides in a[1]
     }
     if (op >= 7 && op <= 9) {
         out[0] = r0;

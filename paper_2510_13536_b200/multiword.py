@@ -57,7 +57,7 @@ def tw_to_fp64(a):
 
 
 OPS = {"add": 0, "mul": 1, "dxmul": 2, "dxadd": 3, "normalize": 4, "div": 5, "neg": 6,
-       "two_sum": 7, "quick_two_sum": 8, "two_prod": 9, "collapse": 10}
+       "two_sum": 7, "quick_two_sum": 8, "two_prod": 9, "collapse": 10, "fma": 11}
 
 
 def scalar_op(op, mode, a, b=None):

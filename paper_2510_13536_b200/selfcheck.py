@@ -51,11 +51,17 @@ def _rel_bits(got, exact, scale=None):
 
 
 def suite_error_free(n=200):
+    from . import eft
     from .multiword import scalar_op
+    out = []
+    try:  # the reference's import-time fused-fma check (eft.py:42-53), on the device
+        eft._check_fused()
+        out.append(CheckResult("error_free", "fused_fma", True, "(1+2^-27)^2 error term exact"))
+    except eft.FmaUnavailableError as exc:
+        out.append(CheckResult("error_free", "fused_fma", False, str(exc)))
     rng = np.random.default_rng(SEED)
     a = rng.standard_normal(n) * np.exp2(rng.integers(-30, 30, n))
     b = rng.standard_normal(n) * np.exp2(rng.integers(-30, 30, n))
-    out = []
     for op, f in (("two_sum", lambda x, y: x + y), ("two_prod", lambda x, y: x * y)):
         bad = 0
         for x, y in zip(a, b):

@@ -52,3 +52,25 @@ def test_neg_sub_and_conversions():
     assert mw.dw_from_fp64(3.0) == (3.0, 0.0) and mw.tw_from_fp64(3.0) == (3.0, 0.0, 0.0)
     assert mw.dw_to_fp64(a) == 1.5 + 2.0 ** -60
     assert mw.qdw_div is mw.dw_div and mw.qtw_div is mw.tw_div
+
+
+@pytest.mark.gpu
+def test_eft_api_golden():
+    """eft.two_sum / quick_two_sum / two_prod_fma against the reference's vectors;
+    eft.fma against glibc's correctly rounded fma (the gmpy2 stand-in)."""
+    import ctypes
+    import ctypes.util
+    from paper_2510_13536_b200 import eft
+    libm = ctypes.CDLL(ctypes.util.find_library("m"))
+    libm.fma.restype = ctypes.c_double
+    libm.fma.argtypes = [ctypes.c_double] * 3
+    for c in OPS["eft"][:80]:
+        a, b = float.fromhex(c["a"]), float.fromhex(c["b"])
+        for name, key in (("two_sum", "two_sum"), ("quick_two_sum", "quick_two_sum"),
+                          ("two_prod_fma", "two_prod")):
+            got = getattr(eft, name)(a, b)
+            assert isinstance(got, eft.Fp64Pair)
+            assert same_bits(np.array(got), arr(c[key])), (name, c["a"], c["b"])
+        assert same_bits([eft.fma(a, b, -a * b)], [libm.fma(a, b, -a * b)])
+    a = 1.0 + 2.0 ** -27
+    assert eft.fma(a, a, -(a * a)) == 2.0 ** -54
