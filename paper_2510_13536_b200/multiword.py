@@ -4,9 +4,36 @@ Only the value containers live on the host; all multi-word ARITHMETIC runs
 on the device (csrc/mw.cuh).  `scalar_op` exposes the device ops one at a
 time for the API and for unit parity tests.
 """
+from fractions import Fraction
 from typing import NamedTuple
 
 import numpy as np
+
+
+def _decimal_str(words, digits):
+    """Exact value of sum(words) in decimal, round-half-even to `digits`
+    significant digits (the reference's ExactValue.decimal_str, its exact-
+    arithmetic module lines 165-188)."""
+    v = sum((Fraction(float(w)) for w in words), Fraction(0))
+    if v == 0:
+        return "0"
+    f, exp10 = abs(v), 0
+    while f >= 10:
+        f /= 10
+        exp10 += 1
+    while f < 1:
+        f *= 10
+        exp10 -= 1
+    scaled = f * Fraction(10) ** (digits - 1)
+    q, r = divmod(scaled.numerator, scaled.denominator)
+    if 2 * r > scaled.denominator or (2 * r == scaled.denominator and q % 2 == 1):
+        q += 1
+    s = str(q)
+    if len(s) > digits:  # rounding carried into a new leading digit
+        s = s[:digits]
+        exp10 += 1
+    body = f"{s[0]}.{s[1:]}" if digits > 1 else s
+    return f"{'-' if v < 0 else ''}{body}e{exp10:+d}"
 
 __all__ = [
     "DoubleWord", "TripleWord", "scalar_op",
@@ -33,6 +60,9 @@ class DoubleWord(NamedTuple):
         a, b = text.split()
         return cls(float.fromhex(a), float.fromhex(b))
 
+    def decimal_str(self, digits=40):
+        return _decimal_str(self, digits)
+
 
 class TripleWord(NamedTuple):
     w0: float
@@ -46,6 +76,9 @@ class TripleWord(NamedTuple):
     def from_hex(cls, text):
         a, b, c = text.split()
         return cls(float.fromhex(a), float.fromhex(b), float.fromhex(c))
+
+    def decimal_str(self, digits=60):
+        return _decimal_str(self, digits)
 
 
 def dw_to_fp64(a):

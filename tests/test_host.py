@@ -189,3 +189,16 @@ def test_compute_without_gpu_fails_loudly():
     from paper_2510_13536_b200 import cg
     with pytest.raises(Exception):
         cg.cg_solve(laplacian_2d(3), np.ones(9), SolverConfig(mode="dw"))
+
+
+def test_decimal_str_matches_reference():
+    """DoubleWord/TripleWord.decimal_str (multiword.py:48-51, 71-75) against the
+    reference's strings (tests/golden/decimal.json)."""
+    from paper_2510_13536_b200.multiword import DoubleWord, TripleWord
+    from tests.golden_io import load
+    for c in load("decimal.json")["cases"]:
+        dw = DoubleWord(*[float.fromhex(v) for v in c["dw"]])
+        tw = TripleWord(*[float.fromhex(v) for v in c["tw"]])
+        assert dw.decimal_str(c["digits"]) == c["dw_str"]
+        assert tw.decimal_str(c["digits"]) == c["tw_str"]
+        assert dw.decimal_str() == c["dw_default"] and tw.decimal_str() == c["tw_default"]
