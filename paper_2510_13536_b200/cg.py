@@ -50,7 +50,7 @@ class SolverConfig:
     normalization: Normalization = Normalization.AFTER_RESIDUAL_AXPY
     history_stride: int = 100
     partitions: int = 1
-    reduction: str = "tile"
+    reduction: Optional[str] = None   # None: "partitions" if partitions != 1 else "tile"
     timing: str = "graph"
 
     def __post_init__(self):
@@ -62,6 +62,11 @@ class SolverConfig:
             raise ValueError("history_stride must be >= 1")
         if self.partitions < 1:
             raise ValueError("partitions must be >= 1")
+        if self.reduction is None:
+            # an explicit partition count asks for the reference's own dot
+            # order (cg.py:42, kernels.py:158-162); the default P = 1 keeps the
+            # fast tile order
+            object.__setattr__(self, "reduction", "partitions" if self.partitions != 1 else "tile")
         if self.reduction not in ("tile", "partitions"):
             raise ValueError(f"unknown reduction {self.reduction!r}")
         if self.timing not in ("graph", "kernels"):
@@ -127,7 +132,7 @@ class Solver:
     def solve(self, b_dev, b_norm, x0_dev=None, xs_dev=None, epsilon=1e-12, max_iterations=None,
               history_stride=100, profile=False):
         max_it = int(max_iterations if max_iterations is not None else 10 * self.n)
-        cap = max_it // history_stride + 4
+        cap = max(max_it, 0) // history_stride + 4
         hk = np.zeros(cap, dtype=np.int64)
         hr = np.zeros(cap)
         ht = np.zeros(cap)
@@ -146,6 +151,7 @@ class Solver:
 
 
 _POOL = None
+_SOLVER_CACHE = 2
 
 
 def _host_pool():
@@ -180,6 +186,17 @@ def cg_solve(A, b, config=SolverConfig(), x0=None, x_star=None, reference=False)
     b = np.ascontiguousarray(b, dtype=np.float64)
     if b.size != A.n_rows:
         raise ValueError("right-hand side length does not match the matrix")
+    # the reference raises these from spmv(A, x0) (kernels.py:181-183) and
+    # from the first history record's residual(x_star, x) (kernels.py:259-260)
+    if x0 is not None:
+        x0 = np.asarray(x0, dtype=np.float64).reshape(-1)
+        if x0.size != A.n_cols:
+            raise ValueError(f"dimension mismatch: matrix has {A.n_cols} columns, "
+                             f"vector has {x0.size} elements")
+    if x_star is not None:
+        x_star = np.asarray(x_star, dtype=np.float64).reshape(-1)
+        if x_star.size != A.n_rows:
+            raise ValueError("dimension mismatch in residual")
     t0 = time.perf_counter()
     # ||b|| is a sequential host sum (the reference order, kernels.py:290-296);
     # it runs on a host thread (ctypes drops the GIL) while the matrix and
@@ -197,13 +214,18 @@ def cg_solve(A, b, config=SolverConfig(), x0=None, x_star=None, reference=False)
             object.__setattr__(A, "_solvers", cache)
         except AttributeError:  # pragma: no cover
             pass
-    solver = cache.get(key)
+    solver = cache.pop(key, None)
     if solver is None:
+        # at most _SOLVER_CACHE solvers per matrix (each holds 4 w n doubles
+        # and a captured graph): a multi-mode run on a large matrix keeps the
+        # most recent ones only
+        while len(cache) >= _SOLVER_CACHE:
+            cache.pop(next(iter(cache)))
         solver = Solver(A, mode, config.normalization, reduction, key[3])
-        cache[key] = solver
+    cache[key] = solver  # most recently used last
     b_dev = _dev_f64(b)
-    x0_dev = None if x0 is None else _dev_f64(np.asarray(x0, dtype=np.float64).reshape(-1))
-    xs_dev = None if x_star is None else _dev_f64(np.asarray(x_star, dtype=np.float64).reshape(-1))
+    x0_dev = None if x0 is None else _dev_f64(x0)
+    xs_dev = None if x_star is None else _dev_f64(x_star)
     bn = bn_future.result()
     profile = config.timing == "kernels"
     res, hist = solver.solve(b_dev, bn, x0_dev, xs_dev, config.epsilon, config.max_iterations,
@@ -217,6 +239,11 @@ def cg_solve(A, b, config=SolverConfig(), x0=None, x_star=None, reference=False)
         ks["spmv"] = res.stage_ms[0] * 1e-3      # SpMV + fused p.q (+ alpha)
         ks["axpy"] = res.stage_ms[1] * 1e-3      # r update + normalize + r.r (+ beta)
         ks["scal_add"] = res.stage_ms[2] * 1e-3  # x update (deferred axpy) + p = r + beta p
+    else:
+        # graph mode: the fused iteration loop is one device region (CUDA
+        # events around each graph launch); it is reported under "spmv", the
+        # kernel that dominates it, so the keys still sum to the device time
+        ks["spmv"] = res.loop_ms * 1e-3
     reason = _lib.STATUS[res.status]
     return SolverResult(converged=reason == "converged", reason=reason,
                         iterations=int(res.iterations),

@@ -103,7 +103,7 @@ __device__ void scalar_init(CgState *st, V<Arith<M>::W> rho) {
         st->iterations = 0;
     } else if (st->max_iters <= 0) {
         st->status = MAX_ITERS;
-        st->iterations = 0;
+        st->iterations = st->max_iters;  // finish(False, "max_iterations", max_iters): cg.py:183
     } else {
         st->status = RUNNING;
     }

@@ -12,7 +12,8 @@ import numpy as np
 from .sparse import CsrMatrix, laplacian_2d
 
 __all__ = ["spmv_fp64_host", "stencil_matrix", "poisson_3d", "config1", "config2",
-           "config3", "config4", "CONFIGS"]
+           "config3", "config4", "config5", "config5_style", "random_irregular_spd",
+           "matrix_digest", "CONFIGS"]
 
 
 def spmv_fp64_host(A, x):
@@ -30,6 +31,18 @@ def spmv_fp64_host(A, x):
         prod = A.values[idx] * x[A.col_idx[idx]]
         y[rows] = y[rows] + prod
     return y
+
+
+def matrix_digest(A):
+    """SHA-256 over (n, row_ptr, col_idx as int64, values): pins a generated
+    problem so a golden recorded against it cannot silently drift."""
+    import hashlib
+    h = hashlib.sha256()
+    h.update(np.int64(A.n_rows).tobytes())
+    h.update(np.ascontiguousarray(A.row_ptr, dtype=np.int64).tobytes())
+    h.update(np.ascontiguousarray(A.col_idx, dtype=np.int64).tobytes())
+    h.update(np.ascontiguousarray(A.values, dtype=np.float64).tobytes())
+    return h.hexdigest()
 
 
 def stencil_matrix(dims, offsets, diag_value, off_value=-1.0):
@@ -158,8 +171,9 @@ def random_irregular_spd(n, seed=3, device="cuda", near_width=1024, cmin=16, cma
     """BASELINE config 5 generator, on the GPU (torch, seeded Philox).
 
     Row i draws c ~ U{cmin..cmax} off-diagonal entries: ceil(c/2) columns
-    within +-near_width of i (clipped), the rest uniform in [0, n); values
-    U(-1, 0); entries landing on the diagonal are dropped.  The pattern is
+    uniform over [i - near_width, i + near_width] clipped to [0, n), minus i;
+    the rest uniform in [0, n); values U(-1, 0); far draws landing on the
+    diagonal are dropped.  The pattern is
     symmetrised by adding (i, j, v) and (j, i, v) and summing duplicates (in
     sorted order, deterministic), then a_ii = 1.01 * sum_j |a_ij| (strictly
     diagonally dominant -> SPD).  Returns a DeviceCsrMatrix (int32 indices).
@@ -176,11 +190,17 @@ def random_irregular_spd(n, seed=3, device="cuda", near_width=1024, cmin=16, cma
     k = torch.arange(T, device=dev) - torch.repeat_interleave(start, cnt)
     near = k < torch.repeat_interleave((cnt + 1) // 2, cnt)
     del k, start
-    d = torch.randint(1, near_width + 1, (T,), generator=g, device=dev)
-    sgn = torch.randint(0, 2, (T,), generator=g, device=dev) * 2 - 1
+    # near: uniform over [i - W, i + W] clipped to [0, n), excluding i
+    lo = (rows - near_width).clamp(min=0)
+    m = (rows + near_width).clamp(max=n - 1) - lo          # candidates (i excluded)
+    u = (torch.rand(T, generator=g, device=dev, dtype=torch.float64) * m).floor().to(torch.int64)
+    u = torch.minimum(u, m - 1)
+    cn = lo + u
+    cn = cn + (cn >= rows).to(torch.int64)
+    del lo, m, u
     far = torch.randint(0, n, (T,), generator=g, device=dev)
-    cols = torch.where(near, (rows + sgn * d).clamp(0, n - 1), far)
-    del d, sgn, far, near
+    cols = torch.where(near, cn, far)
+    del cn, far, near
     vals = -torch.rand(T, generator=g, device=dev, dtype=torch.float64)
     keep = cols != rows
     rows, cols, vals = rows[keep], cols[keep], vals[keep]
@@ -255,4 +275,17 @@ def config5(n=16_000_000, seed=3):
     return dict(name="C5", A=A, b=b, x_star=None, epsilon=1e-12, max_iterations=20000)
 
 
-CONFIGS = {"C1": config1, "C2": config2, "C3": config3, "C4": config4, "C5": config5}
+def config5_style(n=1_000_000, seed=3):
+    """A C5-style instance small enough for a CPU solve of the reference order
+    (parity at scale, tests/golden/scale.json): the config-5 generator run on the host (torch
+    CPU generator -- deterministic, but a different stream from the CUDA
+    one, so this is a different matrix from a device-built C5 of the same
+    n), b ~ U(-1,1) from default_rng(seed); eps 1e-12."""
+    rp, col, val = random_irregular_spd(n, seed=seed, device="cpu")
+    A = CsrMatrix(n, n, rp.numpy().astype(np.int64), col.numpy().astype(np.int64), val.numpy())
+    b = np.random.default_rng(seed).uniform(-1.0, 1.0, n)
+    return dict(name="C5s", A=A, b=b, x_star=None, epsilon=1e-12, max_iterations=20000)
+
+
+CONFIGS = {"C1": config1, "C2": config2, "C3": config3, "C4": config4, "C5": config5,
+           "C5s": config5_style}
