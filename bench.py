@@ -53,15 +53,17 @@ def parse():
     ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4"])
     ap.add_argument("--mode", default="dw", choices=MODES)
     ap.add_argument("--no-per-arith", action="store_true")
-    ap.add_argument("--extra-configs", default="",
-                    help="comma list of other BASELINE configs (C1,C3,C4) to solve once per "
-                         "arithmetic and report under 'configs' (not part of value)")
+    ap.add_argument("--extra-configs", default="C1,C3,C4,C5",
+                    help="comma list of other BASELINE configs to time per arithmetic and "
+                         "report under 'configs' (not part of value); '' for none")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--partitioned", action="store_true",
                     help="force the row-partitioned NCCL path (also at N=1 under torchrun)")
     ap.add_argument("--replicas", action="store_true",
                     help="N>1: independent replicas instead of the row-partitioned solver")
+    ap.add_argument("--c5-rows", type=int, default=16_000_000,
+                    help="rows of the C5 problem of the partitioned (N>1) run")
     return ap.parse_args()
 
 
@@ -157,7 +159,9 @@ def load_problem(name):
 def workload_name(cfg, mode):
     A = cfg["A"]
     desc = {"C1": "2-D 5-point Poisson 256^2", "C2": "3-D 7-point Poisson 128^3",
-            "C3": "3-D 27-point stencil 160^3", "C4": "banded ill-conditioned SPD n=1e6"}[cfg["name"]]
+            "C3": "3-D 27-point stencil 160^3", "C4": "banded ill-conditioned SPD n=1e6",
+            "C5": "random irregular SPD n=16e6 (GPU-built)",
+            "C5s": "random irregular SPD (host-built)"}[cfg["name"]]
     return f"{cfg['name']} {desc}, CG in {mode.upper()} to {cfg['epsilon']:g} (n={A.n_rows}, nnz={A.nnz})"
 
 
@@ -219,6 +223,65 @@ def _free_port():
     port = s.getsockname()[1]
     s.close()
     return port
+
+
+# per config: modes solved to the config's epsilon (full), the rest timed on
+# a bounded sample of unconditional iterations (their full solves take
+# minutes: C4 TW ~1.4e5 iterations)
+EXTRA_PLAN = {"C1": {"full": MODES}, "C3": {"full": MODES},
+              "C4": {"full": ("fp64", "dw", "qtw"), "sample": 3000},
+              "C5": {"full": ("dw", "qtw")}}
+
+
+def extra_config(name, hbm, fp64_peak, torch):
+    """One BASELINE config on one GPU: per arithmetic µs per iteration,
+    iterations to solution, roofline fractions (9-pass bytes / counted FP64
+    ops).  C5 here is the N=1 point of the N>1 strong-scaling run."""
+    from paper_2510_13536_b200 import _lib, kernels
+    from paper_2510_13536_b200.cg import Solver, _b_norm
+    t0 = time.perf_counter()
+    ec = load_problem(name)
+    EA, Eb = ec["A"], ec["b"]
+    en, ennz = EA.n_rows, EA.nnz
+    ebd = torch.from_numpy(Eb).cuda()
+    ebn = _b_norm(Eb)
+    gen_s = time.perf_counter() - t0
+    plan = EXTRA_PLAN.get(name, {"full": MODES})
+    modes = plan["full"] + tuple(m for m in MODES if m not in plan["full"] and plan.get("sample")
+                                 and name != "C5")
+    stride = 10 ** 9
+    rows = {}
+    for m in modes:
+        sv = Solver(EA, m)
+        full = m in plan["full"]
+        eps, mx = (ec["epsilon"], ec["max_iterations"]) if full else (1e-300, plan["sample"])
+        sv.solve(ebd, ebn, None, None, 1e-300, 5, stride)   # warm-up: 5 iterations
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        r, _ = sv.solve(ebd, ebn, None, None, eps, mx, stride)
+        e1.record()
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1) * 1e-3
+        it = max(1, int(r.iterations))
+        wm = WORDS[m]
+        bw = algorithmic_bytes(en, ennz, wm) * it / t / 1e9
+        fn, fx = FLOPS[m]
+        fl = (fn * ennz + fx * en) * it / t
+        rows[m] = {"iterations": int(r.iterations), "reason": _lib.STATUS[r.status],
+                   "final_rel": r.final_rel, "solve": "full" if full else f"{mx} unconditional iterations",
+                   "time_s": t, "us_per_iter": 1e6 * t / it, "hbm_frac": bw / hbm,
+                   "fp64_frac": fl / fp64_peak, "roofline_frac": max(bw / hbm, fl / fp64_peak),
+                   "bound": "fp64" if fl / fp64_peak > bw / hbm else "hbm",
+                   "kernels": sv.describe()}
+        del sv
+        torch.cuda.empty_cache()
+    out = {"workload": workload_name(ec, "all"), "n": en, "nnz": ennz, "generate_s": gen_s,
+           "col_bytes": kernels.device_matrix(EA).col_bytes(), "per_arithmetic": rows}
+    if name == "C5":
+        out["note"] = ("N=1 point of the strong-scaling run (bench.py --gpus N>1: same matrix, "
+                       "same full DW solve, row-partitioned)")
+    return out
 
 
 def run_ours(a):
@@ -381,36 +444,11 @@ def run_ours(a):
     # ---- other BASELINE configs (reported, not part of value) ---------------
     extra = {}
     for name in [c for c in a.extra_configs.split(",") if c]:
-        ec = load_problem(name)
-        EA, Eb = ec["A"], ec["b"]
-        en, ennz = EA.n_rows, EA.nnz
-        ebd = torch.from_numpy(Eb).cuda()
-        ebn = _b_norm(Eb)
-        rows = {}
-        for m in MODES:
-            sv = Solver(EA, m)
-            r0, _ = sv.solve(ebd, ebn, None, None, ec["epsilon"], ec["max_iterations"], stride)
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            r, _ = sv.solve(ebd, ebn, None, None, ec["epsilon"], ec["max_iterations"], stride)
-            e1.record()
-            torch.cuda.synchronize()
-            t = e0.elapsed_time(e1) * 1e-3
-            it = max(1, int(r.iterations))
-            wm = WORDS[m]
-            bw = algorithmic_bytes(en, ennz, wm) * it / t / 1e9
-            fn, fx = FLOPS[m]
-            fl = (fn * ennz + fx * en) * it / t
-            rows[m] = {"iterations": int(r.iterations), "reason": _lib.STATUS[r.status],
-                       "final_rel": r.final_rel, "time_to_solution_s": t,
-                       "us_per_iter": 1e6 * t / it, "hbm_frac": bw / hbm,
-                       "fp64_frac": fl / fp64_peak, "roofline_frac": max(bw / hbm, fl / fp64_peak)}
-            del sv
-            torch.cuda.empty_cache()
-        extra[name] = {"workload": workload_name(ec, "all"), "n": en, "nnz": ennz,
-                       "col_bytes": kernels.device_matrix(EA).col_bytes(), "per_arithmetic": rows}
-        del ec, EA, Eb, ebd
+        try:
+            extra[name] = extra_config(name, hbm, fp64_peak, torch)
+        except Exception as exc:  # pragma: no cover - reported, never fatal
+            extra[name] = {"error": f"{type(exc).__name__}: {exc}"}
+        torch.cuda.empty_cache()
 
     # ---- e2e through the public API with host inputs -------------------------
     e2e = None
@@ -499,33 +537,52 @@ def run_ours(a):
 
 
 def run_partitioned(a, world, rank, local, dist, torch):
-    """Row-partitioned CG over NCCL, weak scaling: the C2
-    Poisson grid grows along z with N (128 x 128 x 128N), each rank owns
-    ~2.1M rows.  value = C2-equivalent CG iterations/s =
-    (global rows x iterations / s) / n(C2), which equals plain iterations/s
-    at N=1."""
+    """Row-partitioned CG over NCCL, STRONG scaling on BASELINE
+    config 5: random irregular SPD, n = 16M, ~1.3e9 nnz, built on every
+    rank's GPU from the same seed (identical matrix), each rank keeping its
+    tile-aligned row block (sliced on the device).  One step = one full CG
+    solve to 1e-12 (a few dozen iterations: 1.01 diagonal dominance keeps C5
+    well conditioned); value = global CG iterations / s (max over ranks).
+    p is all-gathered each iteration (C5's random columns leave no interior
+    tiles to overlap), the tile partials gathered in one
+    all-gather and reduced in the canonical order on every rank."""
     from paper_2510_13536_b200 import problems
     from paper_2510_13536_b200.cg import _b_norm
     from paper_2510_13536_b200.dist import (RankSolver, TorchDistExchange, dist_cg_solve,
                                             local_rows, partition)
     mode = a.mode
-    A = problems.stencil_matrix((128 * world, 128, 128),
-                                [(-1, 0, 0), (0, -1, 0), (0, 0, -1), (0, 0, 1), (0, 1, 0), (1, 0, 0)],
-                                6.0)
-    n = A.n_rows
-    b = problems.spmv_fp64_host(A, np.ones(n))
+    n = a.c5_rows
+    t0 = time.perf_counter()
+    Afull = problems.random_irregular_spd(n, seed=3)
+    nnz = Afull.nnz
+    b = np.random.default_rng(3).uniform(-1.0, 1.0, n)
     bn = _b_norm(b)
     part = partition(n, world)
     lo, hi = part.rows(rank)
-    rs = RankSolver(local_rows(A, lo, hi), part, rank, mode)
-    b_loc = torch.from_numpy(np.ascontiguousarray(b[lo:hi])).cuda()
+    Aloc = local_rows(Afull, lo, hi)
+    Aloc.row_ptr, Aloc.col_idx, Aloc.values = (Aloc.row_ptr.clone(), Aloc.col_idx.clone(),
+                                               Aloc.values.clone())
+    del Afull
+    torch.cuda.empty_cache()
+    rs = RankSolver(Aloc, part, rank, mode)
+    del Aloc
+    torch.cuda.empty_cache()
+    setup_s = time.perf_counter() - t0
+    b_loc = torch.from_numpy(np.ascontiguousarray(b[lo:hi])).cuda() if hi > lo else \
+        torch.zeros(1, dtype=torch.float64, device="cuda")
     ex = TorchDistExchange()
     eps, max_it = 1e-12, 20000
+    seg = [8]
 
     def solve():
         rs.start(b_loc, bn, None, eps, max_it)
-        return dist_cg_solve([rs], ex, bn, eps, max_it, check_every=32, graph=True)
+        # eager stages (each iteration's GPU work, ~ms, dwarfs the host's
+        # launch cost); after the first solve the segment length is the known
+        # iteration count, so a step runs exactly the solve's iterations
+        return dist_cg_solve([rs], ex, bn, eps, max_it, check_every=seg[0], graph=False)
 
+    first = solve()
+    seg[0] = max(1, first.iterations)
     with ClockSampler(local) as clk:
         for _ in range(max(3, a.warmup)):
             solve()
@@ -542,7 +599,7 @@ def run_partitioned(a, world, rank, local, dist, torch):
         e1.record()
         torch.cuda.synchronize()
     dt = e0.elapsed_time(e1) * 1e-3
-    # e2e: the same solves with this rank's b copied in from pinned host
+    # e2e: the same steps with this rank's b copied in from pinned host
     # memory and its solution words copied back every step
     b_host = torch.from_numpy(np.ascontiguousarray(b[lo:hi])).pin_memory()
     x_host = torch.empty(tuple(rs.solution().shape), dtype=torch.float64).pin_memory()
@@ -552,7 +609,8 @@ def run_partitioned(a, world, rank, local, dist, torch):
     e2.record()
     its_e = 0
     for _ in range(a.steps):
-        b_loc.copy_(b_host, non_blocking=True)
+        if hi > lo:
+            b_loc.copy_(b_host, non_blocking=True)
         its_e += solve().iterations
         x_host.copy_(rs.solution(), non_blocking=True)
     e3.record()
@@ -560,28 +618,38 @@ def run_partitioned(a, world, rank, local, dist, torch):
     dte = e2.elapsed_time(e3) * 1e-3
     t = torch.tensor([dt, dte], dtype=torch.float64, device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    dt, dte = float(t[0].item()), float(t[1].item())
-    n_c2 = 128 ** 3
-    value = n * its / dt / n_c2
+    dt, dte = (float(v) for v in t.tolist())
+    w = WORDS[mode]
+    hbm, hbm_src = peaks()
+    value = its / dt
+    per_gpu_bytes = algorithmic_bytes(n, nnz, w) / world
     if rank == 0:
         line = {
-            "metric": "CG iterations/s", "value": value, "unit": "iter/s (C2-equivalent)",
+            "metric": "CG iterations/s", "value": value, "unit": "iter/s",
             "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
-            "ms_per_step": 1e3 * dt / a.steps, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": 1e3 * dt / a.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"3-D 7-point Poisson 128x128x{128 * world} (C2 per GPU), CG in "
-                                   f"{mode.upper()} to 1e-12, row-partitioned",
-                       "n": n, "nnz": A.nnz, "mode": mode,
-                       "iterations_per_solve": its // a.steps,
+            "config": {"workload": f"C5 random irregular SPD n={n} (nnz={nnz}), CG in {mode.upper()}, "
+                                   f"row-partitioned over {world} GPU(s)",
+                       "n": n, "nnz": nnz, "mode": mode, "epsilon": eps,
+                       "step": "one full CG solve to 1e-12",
+                       "iterations_per_solve": r.iterations, "reason": r.reason,
+                       "final_rel": r.final_recurrence_residual,
+                       "time_to_solution_s": dt / a.steps,
                        "parallelism": f"row partition over {world} GPUs: p exchange = NCCL "
                                       f"{'neighbour halo (send/recv)' if ex.mode == 'halo' else 'all-gather'}"
-                                      " + tile-partial all-gather, canonical reduction",
-                       "p_exchange": ex.mode,
-                       "value_definition": "global rows x iterations / s / 128^3"},
-            "e2e": {"value": n * its_e / dte / n_c2, "unit": "iter/s (C2-equivalent)",
+                                      " + one tile-partial all-gather per dot, canonical MW reduction",
+                       "p_exchange": ex.mode, "interior_tiles": list(rs.interior),
+                       "setup_s": setup_s,
+                       "scaling_base": "the N=1 default run reports the same C5 solve under configs.C5"},
+            "roofline": {"bound": "hbm", "unit": "GB/s", "peak": hbm, "peak_source": hbm_src,
+                         "achieved": per_gpu_bytes * its / dt / 1e9,
+                         "frac": per_gpu_bytes * its / dt / 1e9 / hbm, "traffic": None,
+                         "kernel": "whole iteration per GPU (canonical 9-pass bytes / N)"},
+            "e2e": {"value": its_e / dte, "unit": "iter/s",
                     "h2d_bytes_per_step": 8 * (hi - lo),
                     "d2h_bytes_per_step": 8 * int(x_host.numel()),
-                    "note": "per rank: b slice in, solution words out"},
+                    "note": "per rank: b slice in, solution words out, every step"},
             "gpu_launches": launches, "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

@@ -153,6 +153,11 @@ int mwcg_solver_run_profiled(mwcg_solver *s, int64_t k_stop, double *ms);
  * launches on a started solver (bench.py's roofline.launch_us). */
 int mwcg_solver_time_k1(mwcg_solver *s, int reps, double *us);
 int mwcg_solver_state(mwcg_solver *s, mwcg_state *out);
+/* Kernel configuration the solver chose (introspection for tests / bench):
+ * out[0] windowed K1 in use (0/1), [1] its values staged in the ring (0/1), [2] ring slots (tiles),
+ * [3] p windows per stage, [4..7] grid of K1 / K2 / K3 / init,
+ * [8] TMA-staged K2, [9] TMA-staged K3.  n: capacity of out. */
+int mwcg_solver_describe(const mwcg_solver *s, int64_t *out, int n);
 /* norm_metrics_tw (kernels.py:305-328) of the current iterate */
 int mwcg_solver_metrics(mwcg_solver *s, double *err, double *true_res);
 /* whole solve with history (ConvergenceRecord, cg.py:58-63, 129-136) */
@@ -162,11 +167,20 @@ int mwcg_cg_solve(mwcg_solver *s, const double *b, double b_norm, const double *
                   int64_t hist_cap, int64_t *h_k, double *h_rel, double *h_true, double *h_err);
 
 /* ---- row-partitioned multi-GPU rank (driven by dist.py) ----
- * A: this rank's rows, GLOBAL column indices.  p_full (w x ldp) and part
- * (w x part_ld) are caller-owned; the caller all-gathers p_full after XPAY
- * and the tile partials before each FINAL stage.  x0 for mwcg_solver_start
- * is the full (ldp) initial guess.  Results are bitwise identical to the
- * 1-GPU tile-order solve. */
+ * A: this rank's rows, GLOBAL column indices.  p_full (ldp records of w
+ * interleaved words) and part are caller-owned; the caller all-gathers
+ * p_full after XPAY (or exchanges the neighbour halos) and the tile partials
+ * before each FINAL stage.  part is RANK-BLOCKED: rank r's tiles occupy one
+ * contiguous block of w * part_tb doubles at r * w * part_tb (word k of its
+ * tile j at + k * part_tb + j), so the partials gather is ONE all-gather.
+ * x0 for mwcg_solver_start is the full (ldp) initial guess.  Results are
+ * bitwise identical to the 1-GPU tile-order solve.
+ *
+ * Overlap of the halo exchange with the SpMV: SPMV_INTERIOR runs the local
+ * tiles [ilo, ihi) set by mwcg_solver_set_interior (tiles whose rows read
+ * only this rank's slice of p -- they need no halo), SPMV_BOUNDARY the rest;
+ * together they are exactly SPMV.  Every row is computed whole in one of
+ * them, so each row's left-to-right sum (kernels.py:175-180) is unchanged. */
 enum {
     MWCG_STAGE_INIT = 0,        /* r = b - q, p = r, r.r partials (after start's SpMV) */
     MWCG_STAGE_FINAL_INIT = 1,  /* canonical reduce of all partials: rho, rel, stop-at-0 */
@@ -174,11 +188,15 @@ enum {
     MWCG_STAGE_FINAL_ALPHA = 3, /* reduce, breakdown test, alpha */
     MWCG_STAGE_UPDATE = 4,      /* x, r update, r.r partials */
     MWCG_STAGE_FINAL_BETA = 5,  /* reduce, rel, stop / breakdown, beta, k++ */
-    MWCG_STAGE_XPAY = 6         /* p slice = r + beta p */
+    MWCG_STAGE_XPAY = 6,        /* p slice = r + beta p */
+    MWCG_STAGE_SPMV_INTERIOR = 7, /* SPMV on the interior tiles only */
+    MWCG_STAGE_SPMV_BOUNDARY = 8  /* SPMV on the remaining tiles */
 };
 int mwcg_solver_create_dist(mwcg_solver **out, const mwcg_matrix *A, const mwcg_solver_config *cfg,
                             double *x, double *p_full, int64_t ldp, int64_t p_off, double *part,
-                            int64_t part_ld, int64_t tile_off, int64_t ntiles_glob, void *stream);
+                            int64_t part_tb, int64_t tile_off, int64_t ntiles_glob, void *stream);
+/* local tile range [ilo, ihi) of SPMV_INTERIOR (0 <= ilo <= ihi <= local tiles) */
+int mwcg_solver_set_interior(mwcg_solver *s, int64_t ilo, int64_t ihi);
 /* stream: NULL = the solver's stream (graph capture passes the capture stream) */
 int mwcg_solver_dist_stage(mwcg_solver *s, int stage, void *stream);
 

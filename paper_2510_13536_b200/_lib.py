@@ -16,7 +16,7 @@ NORM_ID = {"none": 0, "after-axpy": 1, "every-op": 2}
 RED_ID = {"tile": 0, "partitions": 1}
 STATUS = {0: "running", 1: "converged", 2: "max_iterations", 3: "breakdown"}
 STAGE = {"init": 0, "final_init": 1, "spmv": 2, "final_alpha": 3, "update": 4, "final_beta": 5,
-         "xpay": 6}
+         "xpay": 6, "spmv_interior": 7, "spmv_boundary": 8}
 ERR_VALUE = 1001
 
 c_i64 = ctypes.c_int64
@@ -89,6 +89,7 @@ SIGNATURES = {
     "mwcg_solver_time_k1": (ctypes.c_int, [c_vp, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]),
     "mwcg_solver_run_profiled": (ctypes.c_int, [c_vp, c_i64, c_dp]),
     "mwcg_solver_state": (ctypes.c_int, [c_vp, ctypes.POINTER(StateC)]),
+    "mwcg_solver_describe": (ctypes.c_int, [c_vp, ctypes.POINTER(ctypes.c_int64), ctypes.c_int]),
     "mwcg_solver_metrics": (ctypes.c_int, [c_vp, c_dp, c_dp]),
     "mwcg_cg_solve": (ctypes.c_int, [c_vp, c_vp, ctypes.c_double, c_vp, c_vp, ctypes.c_double,
                                      c_i64, c_i64, ctypes.c_int, ctypes.POINTER(SolveResultC),
@@ -98,6 +99,7 @@ SIGNATURES = {
                                                ctypes.POINTER(SolverConfigC), c_vp, c_vp, c_i64,
                                                c_i64, c_vp, c_i64, c_i64, c_i64, c_vp]),
     "mwcg_solver_dist_stage": (ctypes.c_int, [c_vp, ctypes.c_int, c_vp]),
+    "mwcg_solver_set_interior": (ctypes.c_int, [c_vp, c_i64, c_i64]),
 }
 
 _lib = None

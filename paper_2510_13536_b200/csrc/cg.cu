@@ -17,6 +17,7 @@
 // Reference-order mode (reduction=partitions, bitwise equal to the reference
 // cg_solve(partitions=P)) replaces the fused tile-tree dots by the reference's
 // P-partition sequential dots (two extra kernels per dot).
+#include <algorithm>
 #include <climits>
 #include <cmath>
 #include <cstdlib>
@@ -29,6 +30,10 @@
 namespace mwcg {
 
 using namespace mw;
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 
 __device__ __forceinline__ void set_cond(cudaGraphConditionalHandle h, int use_cond, unsigned v) {
     if (use_cond) cudaGraphSetConditional(h, v);
@@ -155,9 +160,17 @@ __device__ __forceinline__ int64_t snake(int64_t t, int64_t ntiles, int dir) {
 // the sectors a random column costs; x, r, q stay in SoA word planes.
 struct Geo {
     int64_t n, ld, ldp, p_off;
-    int64_t ntiles, tile_off, part_ld, ntiles_glob;
+    int64_t ntiles, tile_off, part_ld, ntiles_glob;  // part_ld: tile block of the partials (common.cuh)
     int final_;
+    // tiles K1 processes: [a0, a1) then [b0, b1) (local indices); all tiles
+    // by default, the interior or the boundary set for the overlapped
+    // multi-GPU SpMV (mwcg_solver_set_interior)
+    int64_t a0, a1, b0, b1;
 };
+__device__ __forceinline__ int64_t k1_count(const Geo &g) { return (g.a1 - g.a0) + (g.b1 - g.b0); }
+__device__ __forceinline__ int64_t k1_tile(const Geo &g, int64_t t) {
+    return t < g.a1 - g.a0 ? g.a0 + t : g.b0 + (t - (g.a1 - g.a0));
+}
 
 // Persistent tile loop: every fused kernel runs grid = min(ntiles, resident
 // CTAs) blocks, block b handling tiles b, b+grid, ...  Partials are indexed by
@@ -210,8 +223,9 @@ __global__ void __launch_bounds__(SpTraits<M>::THREADS, SpTraits<M>::MINB)
     const bool norm_all = st->norm_all != 0;
     const int64_t n = g.n;
     const int dir = (int)(st->k & 1);
-    for (int64_t t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
-        const int64_t tile = snake(t, g.ntiles, dir);
+    const int64_t cnt = k1_count(g);
+    for (int64_t t = blockIdx.x; t < cnt; t += gridDim.x) {
+        const int64_t tile = k1_tile(g, snake(t, cnt, dir));
         // the next row's slice words are loaded while this row walks (they
         // head its dependency chain)
         SliceWords nsw = slice_words(A, tile * TILE + threadIdx.x);
@@ -253,7 +267,232 @@ __global__ void __launch_bounds__(SpTraits<M>::THREADS, SpTraits<M>::MINB)
         }
         if (FUSED) {
             acc = block_tree_first<M, TILE_THREADS>(acc, smem);
-            if (threadIdx.x == 0) store<W>(part, g.part_ld, g.tile_off + tile, acc);
+            if (threadIdx.x == 0) store_part<W>(part, g.part_ld, g.tile_off + tile, acc);
+        }
+    }
+    if (!FUSED || !g.final_) return;
+    if (!last_block_done(&st->ticket[0], &s_last)) return;
+    V<W> pq = reduce_partials_first<M>(part, g.part_ld, g.ntiles_glob, smem);
+    if (threadIdx.x == 0) {
+        st->ticket[0] = 0u;
+        scalar_alpha<M>(st, pq, h, use_cond);
+    }
+}
+
+// ---------------------------------------------------------------- K1W
+// Windowed K1 for the slice-shared-offset layout (stencils, bands: C1-C4).
+// The tile's rows are processed in stages of R rows (R = 256, 512 or 1024).
+// A producer warp brings everything a stage reads into a shared-memory ring
+// with 1-D bulk copies (cp.async.bulk, mbarrier per stage):
+//   * the stage's slice descriptors and its matrix values (contiguous),
+//   * the windows of p the stage gathers from: the distinct column offsets
+//     of the matrix, clustered (offsets closer than R + 4 share a cluster),
+//     give one contiguous window per cluster, [g0 + omin_j, g0 + R - 1 +
+//     omax_j] for a stage starting at global row g0.
+// The consumer threads (256 or 512) then walk their rows with every operand in shared
+// memory: a row's dependency chain is the L1-resident slot word -> a shared
+// load -> the FP64 chain, instead of descriptor (L2) -> pattern (L1) ->
+// gather of p (L2) with HBM values in between (round 1: K1 was latency-bound
+// on that chain, DESIGN.md §3 item 1).  The p.q terms are reduced in the
+// canonical tile order and each row's left-to-right sum is unchanged --
+// results are bitwise K1's.
+constexpr int K1W_MAXCLU = 16;
+constexpr int K1W_MAXNS = 8;
+
+struct WinPlan {
+    int NS, nclu, vs;                // ring slots (whole tiles), p windows, values staged
+    int stage_doubles;               // one ring stage
+    int val_off, win_off, desc_off;  // section offsets (doubles) in a stage
+    int sd0;                         // shared index delta of the diagonal record
+    int omin[K1W_MAXCLU], pre[K1W_MAXCLU], span[K1W_MAXCLU];
+    const uint2 *tab;                // per pattern slot: {lane mask, shared index delta}
+};
+
+// named barriers of K1W (0 is __syncthreads)
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// block tree over the first NT threads, synchronised with named barrier 1
+// (the producer warp and any further consumers do not take part)
+template <int M, int NT>
+__device__ __forceinline__ V<Arith<M>::W> block_tree_bar(V<Arith<M>::W> v, double *smem) {
+    using Ar = Arith<M>;
+    constexpr int W = Ar::W;
+    constexpr int NW = NT / 32;
+    v = warp_tree<M>(v);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < W; k++) smem[k * NW + wid] = v.w[k];
+    }
+    named_bar(1, NT);
+    if (wid == 0) {
+        V<W> u = zero<W>();
+        if (lane < NW) {
+#pragma unroll
+            for (int k = 0; k < W; k++) u.w[k] = smem[k * NW + lane];
+        }
+#pragma unroll
+        for (int off = NW / 2; off >= 1; off >>= 1) u = Ar::add(u, shfl_down<W>(u, off));
+        v = u;
+    }
+    named_bar(1, NT);
+    return v;
+}
+
+template <int W>
+__device__ __forceinline__ V<W> ld_rec(const double *base, int idx) {
+    V<W> r;
+    if (W == 2) {
+        const double2 t = *reinterpret_cast<const double2 *>(base + 2 * idx);
+        r.w[0] = t.x;
+        r.w[W - 1] = t.y;
+    } else {
+#pragma unroll
+        for (int k = 0; k < W; k++) r.w[k] = base[W * idx + k];
+    }
+    return r;
+}
+
+// One thread per row of the tile: 1024 threads (32 warps), row c of every
+// tile the CTA walks is thread c's.  A ring of NS whole-tile slots; thread 0
+// refills a slot with the CTA's tile NS ahead once every thread is done with
+// it (two CTA barriers per tile), so NS - 1 tiles of operands are in flight
+// while one is computed.  A slot holds the tile's slice descriptors, the p
+// windows and -- when they fit (VS: values staged; stencils with few slots)
+// -- the tile's matrix values; otherwise the values stream straight from HBM
+// (ld.global.cs, all U loads of a chunk in flight per thread).  The p.q
+// terms are replayed by the first 256 threads in the canonical order from
+// the q just written (global, this CTA's own stores) and p (the window).
+constexpr int K1W_THREADS = TILE;
+
+template <int M, bool VS>
+struct K1wTraits {
+    static constexpr int U = VS ? 4 : 8;
+};
+
+template <int M, bool FUSED, bool VS>
+__global__ void __launch_bounds__(K1W_THREADS, 1)
+    cg_spmv_pq_win(SellMatrix A, const double *__restrict__ p, double *__restrict__ q, Geo g,
+                   double *__restrict__ part, CgState *st, WinPlan wp, cudaGraphConditionalHandle h,
+                   int use_cond) {
+    using Ar = Arith<M>;
+    constexpr int W = Ar::W;
+    constexpr int U = K1wTraits<M, VS>::U;
+    constexpr uint64_t LO = (1ull << 36) - 1;
+    extern __shared__ __align__(128) double ring[];
+    __shared__ uint64_t full[K1W_MAXNS];
+    __shared__ double smem[W * TILE_THREADS / 32];
+    __shared__ int s_last;
+    if (stopped_k1(st, h, use_cond)) return;
+    const bool norm_all = st->norm_all != 0;
+    const int64_t n = g.n;
+    const int dir = (int)(st->k & 1);
+    const int NS = wp.NS;
+    const int64_t cnt = k1_count(g);
+    const int64_t nmine = cnt > blockIdx.x ? (cnt - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const int c = threadIdx.x, lane = c & 31;
+    const int64_t ldp_even = (g.ldp + 1) & ~(int64_t)1;
+    constexpr int ND = TILE / SLICE + 2;  // descriptors per slot (even count)
+    // slot refill (thread 0): descriptors, [values], p windows of tile tix
+    auto issue = [&](int64_t tix) {
+        const int sidx = (int)(tix % NS);
+        double *stg = ring + (size_t)sidx * wp.stage_doubles;
+        const int64_t tile = k1_tile(g, snake(blockIdx.x + tix * gridDim.x, cnt, dir));
+        const int64_t r0 = tile * TILE;
+        const int64_t sl0 = r0 >> 5;
+        const int64_t sl1 = min(sl0 + TILE / SLICE, A.n_slices);
+        const int64_t v0 = (int64_t)(__ldg((const unsigned long long *)A.slice_ptr + sl0) & LO) << 5;
+        const int64_t v1 = (int64_t)(__ldg((const unsigned long long *)A.slice_ptr + sl1) & LO) << 5;
+        const int64_t g0 = A.row_base + r0;
+        // window j: global records [lo, hi) clipped to [0, ldp), widened to
+        // even records (16-B aligned copies; pre[j] keeps the shared
+        // position's parity equal to the global one)
+        auto win = [&](int j, int64_t &lo, int64_t &clo, int64_t &chi) {
+            lo = g0 + wp.omin[j];
+            const int64_t hi = g0 + TILE + wp.omin[j] + wp.span[j];
+            clo = max(lo, (int64_t)0) & ~(int64_t)1;
+            chi = min((min(hi, g.ldp) + 1) & ~(int64_t)1, ldp_even);
+        };
+        uint32_t bytes = (uint32_t)(ND * 8) + (VS ? (uint32_t)((v1 - v0) * 8) : 0u);
+        for (int j = 0; j < wp.nclu; j++) {
+            int64_t lo, clo, chi;
+            win(j, lo, clo, chi);
+            if (chi > clo) bytes += (uint32_t)((chi - clo) * 8 * W);
+        }
+        const uint64_t pol_stream = l2_policy_evict_first(), pol_keep = l2_policy_evict_last();
+        mbar_arrive_expect_tx(&full[sidx], bytes);
+        bulk_g2s(stg + wp.desc_off, A.slice_ptr + sl0, (uint32_t)(ND * 8), &full[sidx]);
+        if (VS && v1 > v0)
+            bulk_g2s_hint(stg + wp.val_off, A.vals + v0, (uint32_t)((v1 - v0) * 8), &full[sidx], pol_stream);
+        for (int j = 0; j < wp.nclu; j++) {
+            int64_t lo, clo, chi;
+            win(j, lo, clo, chi);
+            if (chi > clo)
+                bulk_g2s_hint(stg + wp.win_off + (int64_t)(j * TILE + wp.pre[j] + (clo - lo)) * W, p + clo * W,
+                              (uint32_t)((chi - clo) * 8 * W), &full[sidx], pol_keep);
+        }
+    };
+    if (c == 0) {
+        for (int i = 0; i < NS; i++) mbar_init(&full[i], 1);
+        mbar_init_fence();
+        for (int64_t i = 0; i < NS && i < nmine; i++) issue(i);
+    }
+    __syncthreads();
+    for (int64_t tix = 0; tix < nmine; tix++) {
+        const int sidx = (int)(tix % NS);
+        const int64_t tile = k1_tile(g, snake(blockIdx.x + tix * gridDim.x, cnt, dir));
+        const int64_t row = tile * TILE + c;
+        mbar_wait(&full[sidx], (uint32_t)((tix / NS) & 1));
+        const double *stg = ring + (size_t)sidx * wp.stage_doubles;
+        const double *sw = stg + wp.win_off;
+        if (row < n) {
+            const uint64_t *dsc = reinterpret_cast<const uint64_t *>(stg + wp.desc_off);
+            const uint64_t d0 = dsc[c >> 5], d1 = dsc[(c >> 5) + 1];
+            const int L = (int)((d1 & LO) - (d0 & LO));
+            const uint2 *tp = wp.tab + (d0 >> 36);
+            const double *vp = VS ? stg + wp.val_off + (((d0 & LO) - (dsc[0] & LO)) << 5) + lane
+                                  : A.vals + ((int64_t)(d0 & LO) << 5) + lane;
+            V<W> sacc = zero<W>();
+            for (int k0 = 0; k0 < L; k0 += U, tp += U, vp += U * SLICE) {
+                uint2 tw[U];
+                double a[U];
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    tw[u] = __ldg(tp + u);
+                    a[u] = VS ? vp[u * SLICE] : ld_stream(vp + u * SLICE);  // (padded past the end)
+                }
+                bool ok[U];
+                V<W> xv[U];
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    ok[u] = (tw[u].x >> lane) & 1u;
+                    xv[u] = ld_rec<W>(sw, c + (ok[u] ? (int)tw[u].y : wp.sd0));
+                }
+#pragma unroll
+                for (int u = 0; u < U; u++)
+                    if (ok[u]) sacc = Ar::add(sacc, Ar::dxmul(a[u], xv[u]));
+            }
+            if (norm_all) sacc = Ar::norm(sacc);
+            store<W>(q, g.ld, row, sacc);
+        }
+        __syncthreads();  // q of the whole tile is written (and visible to the CTA)
+        if (FUSED && c < TILE_THREADS) {
+            V<W> acc = zero<W>();
+#pragma unroll
+            for (int j = 0; j < TILE_ELEMS; j++) {
+                const int cc = c + j * TILE_THREADS;
+                const int64_t rr = tile * TILE + cc;
+                if (rr < n) acc = Ar::add(acc, Ar::mul(ld_rec<W>(sw, cc + wp.sd0), load<W>(q, g.ld, rr)));
+            }
+            const V<W> tot = block_tree_bar<M, TILE_THREADS>(acc, smem);
+            if (c == 0) store_part<W>(part, g.part_ld, g.tile_off + tile, tot);
+        }
+        __syncthreads();  // slot sidx is free
+        if (c == 0 && tix + NS < nmine) {
+            fence_proxy_async_smem();
+            issue(tix + NS);
         }
     }
     if (!FUSED || !g.final_) return;
@@ -336,7 +575,7 @@ __global__ void __launch_bounds__(TILE_THREADS, Hoist<M>::MINB)
         }
         if (FUSED) {
             acc = block_tree<M, TILE_THREADS>(acc, smem);
-            if (threadIdx.x == 0) store<W>(part, g.part_ld, g.tile_off + tile, acc);
+            if (threadIdx.x == 0) store_part<W>(part, g.part_ld, g.tile_off + tile, acc);
         }
     }
     if (!FUSED || !g.final_) return;
@@ -490,10 +729,6 @@ struct XpTma {
     static constexpr size_t SMEM = sizeof(double) * STAGE * NS;
 };
 
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
 // issue the bulk copies of one tile: NP word-plane groups of W planes
 // (srcs[0..NP-1]) then, if pl, the AoS slice of p; a partial tile arrives
 // without transactions
@@ -581,7 +816,7 @@ __global__ void __launch_bounds__(TILE_THREADS, UpTma<M>::MINB)
         }
         if (FUSED) {
             acc = block_tree<M, TILE_THREADS>(acc, smem);
-            if (threadIdx.x == 0) store<W>(part, g.part_ld, g.tile_off + tile, acc);
+            if (threadIdx.x == 0) store_part<W>(part, g.part_ld, g.tile_off + tile, acc);
         }
     }
     if (!FUSED || !g.final_) return;
@@ -695,7 +930,7 @@ __global__ void __launch_bounds__(TILE_THREADS)
         }
         if (FUSED) {
             acc = block_tree<M, TILE_THREADS>(acc, smem);
-            if (threadIdx.x == 0) store<W>(part, g.part_ld, g.tile_off + tile, acc);
+            if (threadIdx.x == 0) store_part<W>(part, g.part_ld, g.tile_off + tile, acc);
         }
     }
     if (!FUSED || !g.final_) return;
@@ -866,6 +1101,12 @@ struct mwcg_solver {
     bool tma = false;                    // TMA-staged K3 (aligned planes; MWCG_TMA=0/1 overrides)
     bool tma2 = false;                   // TMA-staged K2 (MWCG_TMA2=0/1 overrides)
     cudaAccessPolicyWindow l2win{};      // K1's persisting-L2 window over p (num_bytes 0: none)
+    const SellMatrixOwned *Mown = nullptr;
+    int64_t ilo = 0, ihi = 0;            // interior tiles of a rank (SPMV_INTERIOR)
+    bool k1w = false;                    // windowed K1 (dia layout; MWCG_K1W=0/1 overrides)
+    WinPlan wp{};
+    size_t k1w_smem = 0;
+    uint2 *wtab = nullptr;               // K1W slot table (device)
 };
 
 namespace {
@@ -873,10 +1114,12 @@ namespace {
 // Stage launchers shared by the graph body, the profiled (kernel-by-kernel)
 // loop and the multi-rank driver.  fused: tile-tree dots inside K1/K2;
 // otherwise the reference-order dots (cg_dot_part + cg_ref_combine).
+inline int64_t k1_count_host(const Geo &g) { return (g.a1 - g.a0) + (g.b1 - g.b0); }
+
 template <int M, bool FUSED>
 void launch_k1(mwcg_solver *s, cudaStream_t st, cudaGraphConditionalHandle h, int use_cond) {
     const Geo &g = s->geo;
-    const unsigned g0 = s->grid[0];
+    const unsigned g0 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(s->grid[0], k1_count_host(g)));
     // K1 carries an L2 access-policy window over p (the gathered vector):
     // a share of p's lines persists in L2 against the matrix stream and the
     // random gathers of irregular matrices (C5: p is twice the L2)
@@ -890,6 +1133,17 @@ void launch_k1(mwcg_solver *s, cudaStream_t st, cudaGraphConditionalHandle h, in
     cfg.attrs = at;
     cfg.numAttrs = s->l2win.num_bytes > 0 ? 1 : 0;
     const double *pc = s->p;
+    if (s->k1w) {
+        cfg.blockDim = dim3(K1W_THREADS);
+        cfg.dynamicSmemBytes = s->k1w_smem;
+        if (s->wp.vs)
+            cudaLaunchKernelEx(&cfg, cg_spmv_pq_win<M, FUSED, true>, s->A, pc, s->q, g, s->part, s->st, s->wp, h,
+                               use_cond);
+        else
+            cudaLaunchKernelEx(&cfg, cg_spmv_pq_win<M, FUSED, false>, s->A, pc, s->q, g, s->part, s->st, s->wp, h,
+                               use_cond);
+        return;
+    }
 #define K1_LAUNCH(CT) \
     cudaLaunchKernelEx(&cfg, cg_spmv_pq<M, FUSED, CT>, s->A, pc, s->q, g, s->part, s->st, h, use_cond)
     if (s->A.dia) K1_LAUNCH(DiaTag);
@@ -993,6 +1247,24 @@ int enqueue_dist_stage(mwcg_solver *s, int stage) {
         break;
     case MWCG_STAGE_FINAL_INIT: cg_finalize<M><<<1, TILE_THREADS, 0, st>>>(s->part, g, s->st, 0); break;
     case MWCG_STAGE_SPMV: launch_k1<M, true>(s, st, h, 0); break;
+    case MWCG_STAGE_SPMV_INTERIOR:
+    case MWCG_STAGE_SPMV_BOUNDARY: {
+        // launch_k1 reads s->geo: swap in the tile subset for this launch
+        const Geo keep = s->geo;
+        if (stage == MWCG_STAGE_SPMV_INTERIOR) {
+            s->geo.a0 = s->ilo;
+            s->geo.a1 = s->ihi;
+            s->geo.b0 = s->geo.b1 = 0;
+        } else {
+            s->geo.a0 = 0;
+            s->geo.a1 = s->ilo;
+            s->geo.b0 = s->ihi;
+            s->geo.b1 = s->ntiles;
+        }
+        if (k1_count_host(s->geo) > 0) launch_k1<M, true>(s, st, h, 0);
+        s->geo = keep;
+        break;
+    }
     case MWCG_STAGE_FINAL_ALPHA: cg_finalize<M><<<1, TILE_THREADS, 0, st>>>(s->part, g, s->st, 1); break;
     case MWCG_STAGE_UPDATE: launch_k2<M, true>(s, st, h, 0); break;
     case MWCG_STAGE_FINAL_BETA: cg_finalize<M><<<1, TILE_THREADS, 0, st>>>(s->part, g, s->st, 2); break;
@@ -1001,6 +1273,90 @@ int enqueue_dist_stage(mwcg_solver *s, int stage) {
     }
     MWCG_CHECK_LAUNCH();
     return 0;
+}
+
+// Plan the windowed K1 (cg_spmv_pq_win) for a dia-layout matrix: cluster
+// the distinct column offsets (offsets closer than a tile share a window),
+// size one whole-tile ring slot (descriptors + windows [+ values]), and take
+// the values into the slot when >= 2 such slots fit `budget` (else they
+// stream from HBM and only windows are staged, >= 2 slots).  Builds the
+// per-slot table {lane mask, shared index delta}.  Returns false when no
+// ring fits (the classic K1 is used).  MWCG_K1W_VS=0/1 forces the variant.
+bool plan_windows(mwcg_solver *s, int W, size_t budget) {
+    const SellMatrixOwned *M = s->Mown;
+    if (!M || !s->A.dia || M->pat_host.empty() || (s->A.row_base & 1)) return false;
+    const std::vector<uint64_t> &pat = M->pat_host;
+    std::vector<int> offs{0};
+    for (uint64_t w : pat)
+        if (w >> 32) offs.push_back((int)(uint32_t)w);
+    std::sort(offs.begin(), offs.end());
+    offs.erase(std::unique(offs.begin(), offs.end()), offs.end());
+    const int64_t ns = s->A.n_slices;
+    auto align16 = [](int64_t d) { return (d + 15) & ~(int64_t)15; };  // doubles -> 128 B
+    WinPlan wp{};
+    std::vector<int> omin, omax;
+    for (int o : offs) {
+        if (omin.empty() || (int64_t)o - omax.back() > TILE + 4) {
+            omin.push_back(o);
+            omax.push_back(o);
+        } else {
+            omax.back() = o;
+        }
+    }
+    if ((int)omin.size() > K1W_MAXCLU) return false;
+    wp.nclu = (int)omin.size();
+    int64_t pre = 1;
+    for (int j = 0; j < wp.nclu; j++) {
+        if (((pre - omin[j]) % 2 + 2) % 2) pre++;  // window j copies start 16-B aligned
+        wp.omin[j] = omin[j];
+        wp.span[j] = omax[j] - omin[j];
+        wp.pre[j] = (int)pre;
+        pre += wp.span[j] + 4;
+    }
+    const int64_t win_recs = (int64_t)wp.nclu * TILE + pre;
+    int64_t vslots = 0;  // most value slots any tile holds
+    for (int64_t sl = 0; sl < ns; sl += TILE / SLICE) {
+        const int64_t e = std::min<int64_t>(sl + TILE / SLICE, ns);
+        vslots = std::max<int64_t>(vslots, (int64_t)((M->desc_host[e] & ((1ull << 36) - 1)) -
+                                                     (M->desc_host[sl] & ((1ull << 36) - 1))));
+    }
+    const char *fv = std::getenv("MWCG_K1W_VS");
+    for (int vs : {1, 0}) {
+        if (fv && std::atoi(fv) != vs) continue;
+        wp.vs = vs;
+        wp.val_off = 0;
+        wp.win_off = vs ? (int)align16(vslots * SLICE + 8 * SLICE) : 0;  // + slack: chunks read past a slice
+        wp.desc_off = (int)(wp.win_off + align16(win_recs * W));
+        wp.stage_doubles = (int)(wp.desc_off + align16(TILE / SLICE + 2));
+        const size_t slot_bytes = sizeof(double) * (size_t)wp.stage_doubles;
+        const int NS = (int)std::min<size_t>(K1W_MAXNS, budget / slot_bytes);
+        if (NS < 2) continue;
+        wp.NS = NS;
+        // shared index delta of every pattern slot (row c reads record c + delta)
+        auto delta = [&](int off) {
+            int j = 0;
+            while (j + 1 < wp.nclu && off > omax[j]) j++;
+            return j * TILE + wp.pre[j] + (off - wp.omin[j]);
+        };
+        wp.sd0 = delta(0);
+        std::vector<uint2> tab(pat.size());
+        for (size_t k = 0; k < pat.size(); k++) {
+            const uint32_t mask = (uint32_t)(pat[k] >> 32);
+            tab[k] = make_uint2(mask, (unsigned)(mask ? delta((int)(uint32_t)pat[k]) : wp.sd0));
+        }
+        if (s->wtab) pool_free(s->wtab, s->stream);
+        s->wtab = nullptr;
+        if (pool_alloc((void **)&s->wtab, sizeof(uint2) * tab.size(), s->stream) != cudaSuccess) return false;
+        if (cudaMemcpyAsync(s->wtab, tab.data(), sizeof(uint2) * tab.size(), cudaMemcpyHostToDevice,
+                            s->stream) != cudaSuccess ||
+            cudaStreamSynchronize(s->stream) != cudaSuccess)
+            return false;
+        wp.tab = s->wtab;
+        s->wp = wp;
+        s->k1w_smem = slot_bytes * (size_t)NS;
+        return true;
+    }
+    return false;
 }
 
 template <int M>
@@ -1055,6 +1411,29 @@ int compute_grids_t(mwcg_solver *s) {
         const char *t2 = std::getenv("MWCG_TMA2");
         s->tma2 = t2 ? t2[0] != '0' : (M != FP64 && M != TW);
     }
+    {
+        // windowed K1 for the slice-shared-offset layout (MWCG_K1W=0/1 overrides)
+        const char *t = std::getenv("MWCG_K1W");
+        s->k1w = false;
+        if (!t || t[0] != '0') {
+            int maxsm = 0;
+            cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+            // dynamic budget: the opt-in maximum less the static shared memory
+            const size_t budget = (size_t)std::max(0, maxsm - 1024);
+            s->k1w = plan_windows(s, Arith<M>::W, budget);
+            if (s->k1w) {
+                // the attribute is per function (shared by every solver of this
+                // mode): always the full budget, never one solver's ring size
+                const int dyn = (int)budget;
+                cudaFuncSetAttribute(cg_spmv_pq_win<M, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+                cudaFuncSetAttribute(cg_spmv_pq_win<M, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+                cudaFuncSetAttribute(cg_spmv_pq_win<M, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+                cudaFuncSetAttribute(cg_spmv_pq_win<M, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+                if (cudaGetLastError() != cudaSuccess) s->k1w = false;
+            }
+        }
+        cudaGetLastError();
+    }
     if (s->fused) {
         MWCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb[0], cg_spmv_pq<M, true, int32_t>,
                                                                 SpTraits<M>::THREADS, 0));
@@ -1096,6 +1475,10 @@ int compute_grids_t(mwcg_solver *s) {
     // slower for the streaming ones; MWCG_GRID_FULL=<mask> overrides
     unsigned full = (M == TW) ? 7u : ((M == QTW) ? 1u : 0u);
     if (const char *t = std::getenv("MWCG_GRID_FULL")) full = (unsigned)std::atoi(t);
+    if (s->k1w) {
+        nb[0] = 1;             // one CTA (ring) per SM, persistent
+        full &= ~1u;
+    }
     for (int i = 0; i < 4; i++) {
         int64_t g = (int64_t)(nb[i] > 0 ? nb[i] : 1) * sms;
         if (g > s->geo.ntiles || ((full >> i) & 1u)) g = s->geo.ntiles;
@@ -1160,6 +1543,7 @@ void free_solver(mwcg_solver *s) {
     pool_free(s->mpart, st);
     pool_free(s->mout, st);
     pool_free(s->mticket, st);
+    pool_free(s->wtab, st);
     delete[] reinterpret_cast<double *>(s->st_host);
     for (auto &e : s->ev)
         if (e) cudaEventDestroy(e);
@@ -1257,6 +1641,7 @@ int mwcg_solver_create(mwcg_solver **out, const mwcg_matrix *A, const mwcg_solve
     }
     auto *s = new mwcg_solver();
     s->A = A->M->view;
+    s->Mown = A->M;
     s->mode = cfg->mode;
     s->W = words_of(cfg->mode);
     s->cfg = *cfg;
@@ -1266,7 +1651,7 @@ int mwcg_solver_create(mwcg_solver **out, const mwcg_matrix *A, const mwcg_solve
     if (const char *u = std::getenv("MWCG_UNROLL")) s->unroll = std::max(1, std::min(16, std::atoi(u)));
     s->parts = s->fused ? 1 : cfg->partitions;
     s->stream = (cudaStream_t)stream;
-    s->geo = Geo{s->n, s->n, s->n, 0, s->ntiles, 0, s->ntiles, s->ntiles, 1};
+    s->geo = Geo{s->n, s->n, s->n, 0, s->ntiles, 0, s->ntiles, s->ntiles, 1, 0, s->ntiles, 0, 0};
     const size_t vbytes = sizeof(double) * (size_t)s->W * (size_t)(s->n > 0 ? s->n : 1);
     int rc = 0;
 #define TRY(call)                                  \
@@ -1285,7 +1670,8 @@ int mwcg_solver_create(mwcg_solver **out, const mwcg_matrix *A, const mwcg_solve
         s->own_x = true;
     }
     TRY(pool_alloc((void **)&s->r, vbytes, s->stream));
-    TRY(pool_alloc((void **)&s->p, vbytes, s->stream));
+    // p: one spare record (K1W's window copies end on an even record)
+    TRY(pool_alloc((void **)&s->p, vbytes + sizeof(double) * (size_t)s->W, s->stream));
     TRY(pool_alloc((void **)&s->q, vbytes, s->stream));
     int64_t np = s->fused ? (s->ntiles > 0 ? s->ntiles : 1) : s->parts;
     TRY(pool_alloc((void **)&s->part, sizeof(double) * 3 * (size_t)np, s->stream));
@@ -1318,12 +1704,13 @@ int mwcg_solver_create(mwcg_solver **out, const mwcg_matrix *A, const mwcg_solve
 }
 
 // Rank of a row partition.  A: the rank's rows with GLOBAL
-// column indices.  p_full: caller-owned (w, ldp) replica of p; part:
-// caller-owned (w, part_ld) tile partials of all ranks.  The caller gathers
-// them between stages (dist.py).
+// column indices.  p_full: caller-owned replica of p (ldp AoS records);
+// part: caller-owned rank-blocked tile partials of all ranks (part_tb tiles
+// per rank block, common.cuh part_index).  The caller gathers them between
+// stages (dist.py).
 int mwcg_solver_create_dist(mwcg_solver **out, const mwcg_matrix *A, const mwcg_solver_config *cfg,
                             double *x, double *p_full, int64_t ldp, int64_t p_off, double *part,
-                            int64_t part_ld, int64_t tile_off, int64_t ntiles_glob, void *stream) {
+                            int64_t part_tb, int64_t tile_off, int64_t ntiles_glob, void *stream) {
     if (!out || !A || !cfg || !x || !p_full || !part) {
         set_error("null argument");
         return MWCG_ERR_VALUE;
@@ -1333,13 +1720,14 @@ int mwcg_solver_create_dist(mwcg_solver **out, const mwcg_matrix *A, const mwcg_
         return MWCG_ERR_VALUE;
     }
     const int64_t n = A->M->view.n_rows;
-    if (p_off < 0 || p_off + n > ldp || tile_off < 0 || tile_off + num_tiles(n) > part_ld ||
-        ntiles_glob > part_ld || A->M->view.n_cols > ldp) {
+    if (p_off < 0 || p_off + n > ldp || tile_off < 0 || part_tb < 1 || num_tiles(n) > part_tb ||
+        tile_off % part_tb != 0 || A->M->view.n_cols > ldp) {
         set_error("distributed solver: inconsistent geometry");
         return MWCG_ERR_VALUE;
     }
     auto *s = new mwcg_solver();
     s->A = A->M->view;
+    s->Mown = A->M;
     s->mode = cfg->mode;
     s->W = words_of(cfg->mode);
     s->cfg = *cfg;
@@ -1351,7 +1739,7 @@ int mwcg_solver_create_dist(mwcg_solver **out, const mwcg_matrix *A, const mwcg_
     s->x = x;
     s->p = p_full;
     s->part = part;
-    s->geo = Geo{n, n, ldp, p_off, s->ntiles, tile_off, part_ld, ntiles_glob, 0};
+    s->geo = Geo{n, n, ldp, p_off, s->ntiles, tile_off, part_tb, ntiles_glob, 0, 0, s->ntiles, 0, 0};
     const size_t vbytes = sizeof(double) * (size_t)s->W * (size_t)(n > 0 ? n : 1);
 #define TRY(call)                                                \
     do {                                                         \
@@ -1389,6 +1777,21 @@ int mwcg_solver_create_dist(mwcg_solver **out, const mwcg_matrix *A, const mwcg_
     return 0;
 }
 
+int mwcg_solver_set_interior(mwcg_solver *s, int64_t ilo, int64_t ihi) {
+    if (!s || !s->dist) {
+        set_error("not a distributed solver");
+        return MWCG_ERR_STATE;
+    }
+    if (ilo < 0 || ihi < ilo || ihi > s->ntiles) {
+        set_error("interior tiles [%lld, %lld) outside [0, %lld)", (long long)ilo, (long long)ihi,
+                  (long long)s->ntiles);
+        return MWCG_ERR_VALUE;
+    }
+    s->ilo = ilo;
+    s->ihi = ihi;
+    return 0;
+}
+
 int mwcg_solver_dist_stage(mwcg_solver *s, int stage, void *stream) {
     if (!s || !s->dist) {
         set_error("not a distributed solver");
@@ -1403,7 +1806,8 @@ int mwcg_solver_dist_stage(mwcg_solver *s, int stage, void *stream) {
     } guard{s, s->stream};
     if (stream) s->stream = (cudaStream_t)stream;
     if (s->n == 0 && (stage == MWCG_STAGE_INIT || stage == MWCG_STAGE_SPMV || stage == MWCG_STAGE_UPDATE ||
-                      stage == MWCG_STAGE_XPAY))
+                      stage == MWCG_STAGE_XPAY || stage == MWCG_STAGE_SPMV_INTERIOR ||
+                      stage == MWCG_STAGE_SPMV_BOUNDARY))
         return 0;  // a rank without rows still takes part in the finalize stages
     switch (s->mode) {
     case FP64: return enqueue_dist_stage<FP64>(s, stage);
@@ -1412,6 +1816,17 @@ int mwcg_solver_dist_stage(mwcg_solver *s, int stage, void *stream) {
     case TW: return enqueue_dist_stage<TW>(s, stage);
     default: return enqueue_dist_stage<QTW>(s, stage);
     }
+}
+
+int mwcg_solver_describe(const mwcg_solver *s, int64_t *out, int n) {
+    if (!s || !out) {
+        set_error("null argument");
+        return MWCG_ERR_VALUE;
+    }
+    const int64_t v[10] = {s->k1w ? 1 : 0, s->k1w ? s->wp.vs : 0, s->k1w ? s->wp.NS : 0, s->k1w ? s->wp.nclu : 0,
+                           s->grid[0], s->grid[1], s->grid[2], s->grid[3], s->tma2 ? 1 : 0, s->tma ? 1 : 0};
+    for (int i = 0; i < n && i < 10; i++) out[i] = v[i];
+    return 0;
 }
 
 int mwcg_solver_destroy(mwcg_solver *s) {

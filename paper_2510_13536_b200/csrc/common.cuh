@@ -172,6 +172,22 @@ __device__ __forceinline__ mw::V<mw::Arith<M>::W> block_tree_first(mw::V<mw::Ari
     return v;
 }
 
+// Tile-partial layout: rank-blocked word planes.  Word k of global tile t
+// lives at part[(t / tb) * (W * tb) + k * tb + t % tb]: the tiles of one rank
+// of a row partition (tb = tiles per rank) form ONE contiguous block of W*tb
+// doubles, so a multi-GPU gather of the partials is a single all-gather; on
+// one GPU tb covers every tile and the layout is plain word planes of
+// leading dimension tb.
+__device__ __forceinline__ int64_t part_index(int64_t tb, int W, int k, int64_t t) {
+    const int64_t blk = t / tb;
+    return blk * (W * tb) + (int64_t)k * tb + (t - blk * tb);
+}
+template <int W>
+__device__ __forceinline__ void store_part(double *part, int64_t tb, int64_t t, mw::V<W> v) {
+#pragma unroll
+    for (int k = 0; k < W; k++) part[part_index(tb, W, k, t)] = v.w[k];
+}
+
 // Thread t of the reducing block accumulates partials t, t+256, t+512, ...
 // in increasing order (the canonical order).  The loads are issued PF at a
 // time before the dependent additions, so the serial tail of the last block
@@ -189,7 +205,7 @@ __device__ __forceinline__ mw::V<mw::Arith<M>::W> accumulate_partials(const doub
         for (int j = 0; j < PF; j++) {
             const int64_t idx = b + (int64_t)j * TILE_THREADS;
 #pragma unroll
-            for (int k = 0; k < W; k++) t[j].w[k] = idx < ntiles ? __ldcg(part + k * ld + idx) : 0.0;
+            for (int k = 0; k < W; k++) t[j].w[k] = idx < ntiles ? __ldcg(part + part_index(ld, W, k, idx)) : 0.0;
         }
 #pragma unroll
         for (int j = 0; j < PF; j++)
@@ -208,7 +224,7 @@ __device__ __forceinline__ mw::V<mw::Arith<M>::W> reduce_partials_first(const do
     return block_tree_first<M, TILE_THREADS>(acc, smem);
 }
 
-// Second pass over ntiles partials (SoA, leading dim ld) by one block of
+// Second pass over ntiles partials (layout above, tile block ld) by one block of
 // TILE_THREADS threads; identical procedure to a tile with E=ceil(ntiles/TB).
 // Partials written by other CTAs in this grid are read with ld.cg (L2) loads.
 template <int M>

@@ -3,6 +3,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <vector>
 #include "common.cuh"
 
 // library error codes (cudaError_t values are returned as-is, all < 1000)
@@ -18,7 +19,14 @@ struct SellMatrixOwned {
     double *vals = nullptr;
     uint64_t *om = nullptr;  // slice-shared-offset pattern table (dia layout)
     int64_t n_patterns_words = 0;
+    // dia layout, host copies: the pattern table and the slice descriptors
+    // (start/32 | base << 36), used to plan the windowed SpMV (cg.cu: K1W)
+    std::vector<uint64_t> pat_host, desc_host;
 };
+
+// slice descriptors are padded with this many copies of the last one, so a
+// bulk copy of a stage's descriptors may run past the last slice
+constexpr int DESC_PAD = 64;
 
 // col_format: -1 auto (slice-shared offsets when they pay, else int16 deltas
 // when they fit, else int32), 0 force int32, 1 force int16, 2 force slice-shared

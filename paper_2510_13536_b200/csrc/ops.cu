@@ -41,7 +41,7 @@ __global__ void __launch_bounds__(TILE_THREADS) dot_tile_kernel(int64_t n, const
         if (i < n) acc = Ar::add(acc, Ar::mul(load_ro<W>(x, ldx, i), load_ro<W>(y, ldy, i)));
     }
     acc = block_tree<M, TILE_THREADS>(acc, smem);
-    if (threadIdx.x == 0) store<W>(part, ntiles, blockIdx.x, acc);
+    if (threadIdx.x == 0) store_part<W>(part, ntiles, blockIdx.x, acc);
     if (!last_block_done(ticket, &s_last)) return;
     V<W> r = reduce_partials_block<M>(part, ntiles, ntiles, smem);
     if (threadIdx.x == 0) {

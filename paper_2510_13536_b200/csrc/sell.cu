@@ -166,9 +166,13 @@ static int dia_patterns(SellMatrixOwned *M, int64_t *slice_ptr, int64_t n_words,
     M->om = nullptr;
     MWCG_CUDA(pool_alloc((void **)&M->om, sizeof(uint64_t) * pat.size(), st));
     MWCG_CUDA(cudaMemcpyAsync(M->om, pat.data(), sizeof(uint64_t) * pat.size(), cudaMemcpyHostToDevice, st));
-    MWCG_CUDA(cudaMemcpyAsync(slice_ptr, desc.data(), sizeof(uint64_t) * (ns + 1), cudaMemcpyHostToDevice, st));
+    desc.resize(ns + 1 + DESC_PAD, desc[ns]);
+    MWCG_CUDA(cudaMemcpyAsync(slice_ptr, desc.data(), sizeof(uint64_t) * desc.size(), cudaMemcpyHostToDevice, st));
     MWCG_CUDA(cudaStreamSynchronize(st));
     M->n_patterns_words = (int64_t)pat.size();
+    M->pat_host = std::move(pat);
+    desc.resize(ns + 1);
+    M->desc_host = std::move(desc);
     return 0;
 }
 
@@ -190,7 +194,7 @@ static int build_dia(SellMatrixOwned *M, const I *rp, const I *ci, const double 
     dia_walk_kernel<I, false><<<blocks, 256, 0, st>>>(rp, ci, va, A.n_rows, A.n_slices, A.row_base, slice_sz,
                                                       nullptr, nullptr, nullptr, flag);
     MWCG_CHECK_LAUNCH();
-    MWCG_CUDA(pool_alloc((void **)&slice_ptr, sizeof(int64_t) * (A.n_slices + 1), st));
+    MWCG_CUDA(pool_alloc((void **)&slice_ptr, sizeof(int64_t) * (A.n_slices + 1 + DESC_PAD), st));
     size_t tmp_bytes = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, slice_sz, slice_ptr, A.n_slices + 1, st);
     void *tmp = nullptr;

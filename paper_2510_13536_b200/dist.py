@@ -9,16 +9,24 @@ ntiles)), i.e. global rows [r*tmax*TILE, ...).  Each rank keeps
   * a full replica of p, shape (R*tmax*TILE, w) -- interleaved words, the
     layout the kernels gather from: the local slice is written by XPAY and the
     replica is refreshed by ONE all-gather of the contiguous slices,
-  * the tile partials of ALL ranks, shape (w, R*tmax): every rank writes its
-    own tiles and an all-gather completes the array.
+  * the tile partials of ALL ranks, rank-blocked, shape (R, w, tmax): every
+    rank writes its own block and ONE all-gather completes the array.
 
-Per iteration:  SpMV(+p.q partials) -> gather partials -> finalize(alpha)
+Per iteration:  [start the p exchange] -> SpMV of the interior tiles (rows
+that read only this rank's slice of p) -> [finish the exchange] -> SpMV of
+the boundary tiles (+p.q partials) -> gather partials -> finalize(alpha)
 -> update(+r.r partials) -> gather partials -> finalize(beta, stop test)
--> XPAY -> gather p.  The finalize stage reduces all global tiles in the
-canonical order on every rank, so alpha/beta/stop decisions are identical on
-all ranks and the whole solve is bitwise identical to the 1-GPU tile-order
-solve.  There is no floating-point all-reduce anywhere (it would
-lose the low words and fix no order).
+-> XPAY.  For the stencil / band configs the p exchange is a neighbour halo
+and runs concurrently with the interior SpMV; a row is always computed whole
+by one of the two SpMV launches, so its left-to-right sum (kernels.py:
+175-180) is unchanged.  C5's random global columns leave no interior tiles:
+its all-gather cannot overlap the SpMV without changing the reference's
+per-row summation order.  The finalize stage reduces all
+global tiles in the canonical order on every rank, so alpha/beta/stop
+decisions are identical on all ranks and the whole solve is bitwise
+identical to the 1-GPU tile-order solve.  There is no floating-point
+all-reduce anywhere (it would lose the low words and fix no
+order).
 
 The exchange is pluggable: `TorchDistExchange` (one rank per process over
 torch.distributed: NCCL on B200 / NVLink, gloo on CPU) or `LocalExchange`
@@ -76,10 +84,69 @@ def partition(n, world):
 
 
 def local_rows(A, lo, hi):
-    """Rows [lo, hi) of A with global column indices."""
+    """Rows [lo, hi) of A with global column indices.  A DeviceCsrMatrix (C5,
+    built on the GPU) is sliced on the device: no host copy of its ~1e9
+    entries."""
+    if isinstance(A.row_ptr, torch.Tensor):
+        from .sparse import DeviceCsrMatrix
+        a, b = int(A.row_ptr[lo]), int(A.row_ptr[hi])
+        rp = (A.row_ptr[lo:hi + 1] - A.row_ptr[lo]).contiguous()
+        return DeviceCsrMatrix(hi - lo, A.n_cols, rp, A.col_idx[a:b], A.values[a:b])
     rp = A.row_ptr[lo:hi + 1] - A.row_ptr[lo]
     a, b = A.row_ptr[lo], A.row_ptr[hi]
     return CsrMatrix(hi - lo, A.n_cols, rp, A.col_idx[a:b], A.values[a:b])
+
+
+def tile_column_ranges(A_local):
+    """(min, max) global column read by each local tile of TILE rows (rows
+    are sorted, so a row's first / last entry hold its extremes); empty tiles
+    give (+inf, -inf) as (n_cols, -1)."""
+    n = A_local.n_rows
+    nt = (n + TILE - 1) // TILE
+    if nt == 0:
+        return np.zeros(0, np.int64), np.zeros(0, np.int64)
+    rp, ci = A_local.row_ptr, A_local.col_idx
+    if isinstance(rp, torch.Tensor):
+        rp64 = rp.to(torch.int64)
+        lens = rp64[1:] - rp64[:-1]
+        nz = lens > 0
+        first = torch.where(nz, ci[rp64[:-1].clamp(max=max(ci.numel() - 1, 0))].to(torch.int64)
+                            if ci.numel() else torch.zeros_like(rp64[:-1]),
+                            torch.full_like(rp64[:-1], A_local.n_cols))
+        last = torch.where(nz, ci[(rp64[1:] - 1).clamp(min=0)].to(torch.int64)
+                           if ci.numel() else torch.zeros_like(rp64[1:]),
+                           torch.full_like(rp64[1:], -1))
+        pad = nt * TILE - n
+        first = torch.nn.functional.pad(first, (0, pad), value=A_local.n_cols)
+        last = torch.nn.functional.pad(last, (0, pad), value=-1)
+        return (first.view(nt, TILE).min(1).values.cpu().numpy(),
+                last.view(nt, TILE).max(1).values.cpu().numpy())
+    rp = np.asarray(rp, dtype=np.int64)
+    lens = np.diff(rp)
+    nz = lens > 0
+    first = np.full(nt * TILE, A_local.n_cols, dtype=np.int64)
+    last = np.full(nt * TILE, -1, dtype=np.int64)
+    if ci.size:
+        first[:n][nz] = ci[rp[:-1][nz]]
+        last[:n][nz] = ci[rp[1:][nz] - 1]
+    return first.reshape(nt, TILE).min(1), last.reshape(nt, TILE).max(1)
+
+
+def interior_tiles(A_local, lo, hi):
+    """The longest run [ilo, ihi) of local tiles whose rows read p only in
+    this rank's own rows [lo, hi): their SpMV needs no exchanged data and
+    overlaps the p exchange."""
+    tmin, tmax_ = tile_column_ranges(A_local)
+    ok = (tmin >= lo) & (tmax_ < hi)
+    best, cur = (0, 0), None
+    for t, good in enumerate(ok):
+        if good:
+            cur = (cur[0], t + 1) if cur else (t, t + 1)
+            if cur[1] - cur[0] > best[1] - best[0]:
+                best = cur
+        else:
+            cur = None
+    return best
 
 
 class RankSolver:
@@ -94,21 +161,24 @@ class RankSolver:
         assert A_local.n_rows == self.n
         self.x = torch.zeros((w, max(self.n, 1)), dtype=torch.float64, device=dev)
         self.p_full = torch.zeros((part.ld_full, w), dtype=torch.float64, device=dev)  # AoS
-        self.partials = torch.zeros((w, part.part_ld), dtype=torch.float64, device=dev)
+        # rank-blocked tile partials (include/mwcg_cuda.h): rank r's block of
+        # w * tmax doubles at r * w * tmax
+        self.partials = torch.zeros(part.world * w * part.tmax, dtype=torch.float64, device=dev)
         self.dm = device_matrix(A_local, row_base=self.lo)
         L = _lib.load()
         self._L = L
         cfg = _lib.SolverConfigC(_lib.MODE_ID[mode], _lib.NORM_ID[normalization], 0, 0, 1)
         h = ctypes.c_void_p()
-        t_lo, _ = part.tiles(rank)
         _lib.check(L.mwcg_solver_create_dist(
             ctypes.byref(h), self.dm.handle, ctypes.byref(cfg), _lib.ptr(self.x),
-            _lib.ptr(self.p_full), part.ld_full, self.lo, _lib.ptr(self.partials), part.part_ld,
-            t_lo, part.ntiles, _lib.stream_handle()))
+            _lib.ptr(self.p_full), part.ld_full, self.lo, _lib.ptr(self.partials), part.tmax,
+            rank * part.tmax, part.ntiles, _lib.stream_handle()))
         self.handle = h
         import weakref
         self._fin = weakref.finalize(self, L.mwcg_solver_destroy, h)
         self.col_range = column_range(A_local)
+        self.interior = interior_tiles(A_local, self.lo, self.hi)
+        _lib.check(L.mwcg_solver_set_interior(h, *self.interior))
 
     def p_rows(self, lo, hi):
         """Contiguous views of the p replica for global rows [lo, hi) (AoS:
@@ -119,18 +189,15 @@ class RankSolver:
     def p_slice(self):
         return self.rank * self.part.nmax, self.part.nmax
 
-    def part_slice(self):
-        return self.rank * self.part.tmax, self.part.tmax
-
     def segments(self, which):
         """1-D (buffer, offset, count) triples this rank contributes to a
-        gather: the AoS p replica is one contiguous block; the SoA tile
-        partials are one block per word plane."""
+        gather: the AoS p replica and the rank-blocked tile partials are one
+        contiguous block each (one all-gather per exchange)."""
         if which == "p":
             off, cnt = self.p_slice()
             return [(self.p_full.view(-1), off * self.w, cnt * self.w)]
-        off, cnt = self.part_slice()
-        return [(self.partials[k], off, cnt) for k in range(self.w)]
+        blk = self.w * self.part.tmax
+        return [(self.partials, self.rank * blk, blk)]
 
     def start(self, b_local, b_norm, x0_full, epsilon, max_iterations):
         self._b = b_local          # keep alive: the device state points at it
@@ -185,7 +252,10 @@ def halo_plan(part, ranges, max_fraction=0.5):
 
 
 class LocalExchange:
-    """R ranks in one process (one GPU): copy each rank's slice to the others."""
+    """R ranks in one process (one GPU): copy each rank's slice to the others.
+    start() does nothing and finish() copies, so the interior SpMV issued
+    between them runs BEFORE the exchanged data lands: a tile wrongly
+    classified as interior would read stale p and break the bitwise tests."""
 
     def __init__(self):
         self.pieces = None
@@ -193,6 +263,12 @@ class LocalExchange:
     def setup(self, ranks):
         self.pieces = halo_plan(ranks[0].part, [rs.col_range for rs in ranks])
         self.mode = "halo" if self.pieces is not None else "allgather"
+
+    def start(self, ranks, which):
+        return (ranks, which)
+
+    def finish(self, handle):
+        self.gather(*handle)
 
     def gather(self, ranks, which):
         if which == "p" and self.pieces is not None:
@@ -241,24 +317,38 @@ class TorchDistExchange:
             elif dst == me.rank:
                 ops += [self.dist.P2POp(self.dist.irecv, seg, src, group=self.group)
                         for seg in me.p_rows(lo, hi)]
-        if ops:
-            for req in self.dist.batch_isend_irecv(ops):
-                req.wait()
+        return self.dist.batch_isend_irecv(ops) if ops else []
 
-    def gather(self, ranks, which):
+    def start(self, ranks, which):
+        """Issue the exchange asynchronously (NCCL runs it on its own stream,
+        ordered after this stream's work so far); finish() makes the current
+        stream wait for it."""
         (me,) = ranks
         if which == "p" and self.pieces is not None:
-            self._halo(me)
-            return
+            return self._halo(me), None
+        works, post = [], []
         for buf, off, cnt in me.segments(which):
             if self.nccl:  # in-place: each rank's slice already sits at off = rank*cnt
-                self.dist.all_gather_into_tensor(buf, buf[off:off + cnt], group=self.group)
+                works.append(self.dist.all_gather_into_tensor(buf, buf[off:off + cnt],
+                                                              group=self.group, async_op=True))
             else:
                 outs = list(buf.split(cnt))
                 tmp = [torch.empty_like(o) for o in outs]
-                self.dist.all_gather(tmp, buf[off:off + cnt].clone(), group=self.group)
-                for o, t in zip(outs, tmp):
-                    o.copy_(t)
+                works.append(self.dist.all_gather(tmp, buf[off:off + cnt].clone(),
+                                                  group=self.group, async_op=True))
+                post.append((outs, tmp))
+        return works, post
+
+    def finish(self, handle):
+        works, post = handle
+        for w in works:
+            w.wait()
+        for outs, tmp in post or ():
+            for o, t in zip(outs, tmp):
+                o.copy_(t)
+
+    def gather(self, ranks, which):
+        self.finish(self.start(ranks, which))
 
 
 @dataclass
@@ -270,12 +360,22 @@ class DistResult:
     launches: int = 0  # kernels one rank launched (start + stages; graph replays counted)
 
 
-STAGES_PER_ITERATION = 5
+def _kernels_per_iteration(rs):
+    """Kernels one rank launches per iteration: SpMV of the interior and of
+    the boundary tiles (each only if non-empty), finalize(alpha), update,
+    finalize(beta), XPAY."""
+    ilo, ihi = getattr(rs, "interior", (0, 0))
+    nt = (rs.n + TILE - 1) // TILE
+    return 4 + (1 if ihi > ilo else 0) + (1 if nt - (ihi - ilo) > 0 else 0)
 
 
 def _iteration(ranks, exchange):
+    h = exchange.start(ranks, "p")       # p slices written by the last XPAY / init
     for rs in ranks:
-        rs.stage("spmv")
+        rs.stage("spmv_interior")        # overlaps the exchange
+    exchange.finish(h)
+    for rs in ranks:
+        rs.stage("spmv_boundary")
     exchange.gather(ranks, "part")
     for rs in ranks:
         rs.stage("final_alpha")
@@ -286,7 +386,6 @@ def _iteration(ranks, exchange):
         rs.stage("final_beta")
     for rs in ranks:
         rs.stage("xpay")
-    exchange.gather(ranks, "p")
 
 
 def dist_cg_solve(ranks, exchange, b_norm, epsilon=1e-12, max_iterations=None,
@@ -305,7 +404,6 @@ def dist_cg_solve(ranks, exchange, b_norm, epsilon=1e-12, max_iterations=None,
     exchange.gather(ranks, "part")
     for rs in ranks:
         rs.stage("final_init")
-    exchange.gather(ranks, "p")
     st = ranks[0].state()
     calls = 0
     cache = getattr(ranks[0], "_graphs", None)
@@ -346,8 +444,8 @@ def dist_cg_solve(ranks, exchange, b_norm, epsilon=1e-12, max_iterations=None,
         calls += check_every
         st = ranks[0].state()
     reason = _lib.STATUS[st.status]
-    # start: x0 spread + SpMV + init stage; final_init; 5 stage kernels per iteration
-    launches = 3 + 1 + STAGES_PER_ITERATION * calls
+    # start: x0 spread + SpMV + init stage; final_init; then the stage kernels
+    launches = 3 + 1 + _kernels_per_iteration(ranks[0]) * calls
     return DistResult(reason == "converged", reason, int(st.iterations), float(st.rel), launches)
 
 

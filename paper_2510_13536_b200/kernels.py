@@ -11,6 +11,7 @@ _fast.py:342-356); `partitions=0` selects the device tile tree (the order the
 fused CG uses).
 """
 import ctypes
+import warnings
 import weakref
 
 import numpy as np
@@ -128,9 +129,12 @@ def device_matrix(A, row_base=0, col_format=-1):
     else:
         # non_blocking: a DMA straight from the caller's buffers when they are
         # pinned (torch checks); pageable buffers fall back to a staged copy
-        rp = torch.from_numpy(np.ascontiguousarray(A.row_ptr, dtype=np.int64)).to(dev, non_blocking=True)
-        ci = torch.from_numpy(np.ascontiguousarray(A.col_idx, dtype=np.int64)).to(dev, non_blocking=True)
-        va = torch.from_numpy(np.ascontiguousarray(A.values, dtype=np.float64)).to(dev, non_blocking=True)
+        # (CsrMatrix arrays are read-only views; torch only reads them here)
+        with warnings.catch_warnings():
+            warnings.filterwarnings("ignore", message="The given NumPy array is not writable")
+            rp = torch.from_numpy(np.ascontiguousarray(A.row_ptr, dtype=np.int64)).to(dev, non_blocking=True)
+            ci = torch.from_numpy(np.ascontiguousarray(A.col_idx, dtype=np.int64)).to(dev, non_blocking=True)
+            va = torch.from_numpy(np.ascontiguousarray(A.values, dtype=np.float64)).to(dev, non_blocking=True)
         ib = 8
     handle = ctypes.c_void_p()
     _lib.check(L.mwcg_matrix_create_ex(ctypes.byref(handle), A.n_rows, A.n_cols, A.nnz,

@@ -23,40 +23,46 @@ class CpuRank:
         self.n = self.hi - self.lo
         self.A = A_local
         self.p_full = torch.zeros((w, part.ld_full), dtype=torch.float64)
-        self.partials = torch.zeros((w, part.part_ld), dtype=torch.float64)
+        # rank-blocked partials, as the product's RankSolver (include/mwcg_cuda.h)
+        self.partials = torch.zeros(part.world * w * part.tmax, dtype=torch.float64)
         self.x = np.zeros((w, self.n))
         self.r = np.zeros((w, self.n))
         self.q = np.zeros((w, self.n))
         quasi = mode in ("qdw", "qtw")
         self.norm_r = quasi and normalization != "none"
         self.norm_all = quasi and normalization == "every-op"
-        self.tile_off = part.tiles(rank)[0]
         self.st = SimpleNamespace(status=0, k=0, iterations=0, rel=0.0)
         ci = A_local.col_idx
         self.col_range = (int(ci.min()), int(ci.max())) if ci.size else (0, -1)
+        from paper_2510_13536_b200.dist import interior_tiles
+        self.interior = interior_tiles(A_local, self.lo, self.hi)
 
     def p_slice(self):
         return self.rank * self.part.nmax, self.part.nmax
-
-    def part_slice(self):
-        return self.rank * self.part.tmax, self.part.tmax
 
     def p_rows(self, lo, hi):  # SoA planes: one contiguous view per word
         return [self.p_full[j, lo:hi] for j in range(self.w)]
 
     def segments(self, which):  # this stand-in keeps p in SoA planes
-        off, cnt = self.p_slice() if which == "p" else self.part_slice()
-        buf = self.p_full if which == "p" else self.partials
-        return [(buf[k], off, cnt) for k in range(self.w)]
+        if which == "p":
+            off, cnt = self.p_slice()
+            return [(self.p_full[k], off, cnt) for k in range(self.w)]
+        blk = self.w * self.part.tmax
+        return [(self.partials, self.rank * blk, blk)]
+
+    def _blocks(self):
+        """(w, R*tmax) word planes of the rank-blocked partials (a view)."""
+        R, w, t = self.part.world, self.w, self.part.tmax
+        return self.partials.view(R, w, t).permute(1, 0, 2).reshape(w, R * t)
 
     def _pl(self):
         return self.p_full.numpy()[:, self.lo:self.hi]
 
     def _partials_of(self, x, y):
-        out = np.ascontiguousarray(self.partials.numpy())
-        orc.tile_partials(self.mode, np.ascontiguousarray(x), np.ascontiguousarray(y), out,
-                          self.tile_off)
-        self.partials.copy_(torch.from_numpy(out))
+        blk = self.w * self.part.tmax
+        out = np.zeros((self.w, self.part.tmax))
+        orc.tile_partials(self.mode, np.ascontiguousarray(x), np.ascontiguousarray(y), out, 0)
+        self.partials[self.rank * blk:(self.rank + 1) * blk].copy_(torch.from_numpy(out).reshape(-1))
 
     def start(self, b_local, b_norm, x0_full, epsilon, max_iterations):
         self.b = np.asarray(b_local, dtype=np.float64)
@@ -76,7 +82,8 @@ class CpuRank:
         return float(orc.scalar_op("collapse", self.mode, v)[0])
 
     def _reduce(self):
-        return orc.reduce_partials(self.mode, self.partials.numpy()[:, :self.part.ntiles])
+        return orc.reduce_partials(self.mode, np.ascontiguousarray(
+            self._blocks().numpy()[:, :self.part.ntiles]))
 
     def stage(self, name):
         st, m = self.st, self.mode
@@ -96,13 +103,25 @@ class CpuRank:
             if st.rel < self.eps:
                 st.status, st.iterations = 1, 0
             elif self.max_it <= 0:
-                st.status, st.iterations = 2, 0
-        elif name == "spmv":
+                st.status, st.iterations = 2, self.max_it
+        elif name in ("spmv", "spmv_interior", "spmv_boundary"):
+            # rows of the interior tiles are computed before the p exchange
+            # lands (dist._iteration): from the stale replica, exactly as the
+            # device does -- a misclassified tile would break the bitwise test
             if self.n:
-                self.q = orc.spmv(m, self.A, self.p_full.numpy())
+                ilo, ihi = self.interior
+                rows = np.zeros(self.n, dtype=bool)
+                rows[ilo * 1024:ihi * 1024] = True
+                if name == "spmv_boundary":
+                    rows = ~rows
+                elif name == "spmv":
+                    rows[:] = True
+                q = orc.spmv(m, self.A, self.p_full.numpy())
                 if self.norm_all:
-                    self.q = orc.normalize(m, self.q)
-                self._partials_of(self._pl(), self.q)
+                    q = orc.normalize(m, q)
+                self.q[:, rows] = q[:, rows]
+                if name != "spmv_interior":
+                    self._partials_of(self._pl(), self.q)
         elif name == "final_alpha":
             pq = self._reduce()
             f = self._coll(pq)

@@ -112,3 +112,29 @@ class TestSolverArgs:
             A.col_idx[0] = 1
         A.release_device()
         assert A._device is None
+
+
+class TestPartitionHelpers:
+    def test_interior_tiles_banded(self):
+        from paper_2510_13536_b200.dist import interior_tiles, local_rows, partition
+        A = laplacian_2d(100)               # bandwidth 100, 10 tiles
+        part = partition(A.n_rows, 2)
+        lo, hi = part.rows(0)
+        assert interior_tiles(local_rows(A, lo, hi), lo, hi) == (0, 4)   # tile 4 reads rank 1
+        lo, hi = part.rows(1)
+        assert interior_tiles(local_rows(A, lo, hi), lo, hi) == (1, 5)   # tile 0 reads rank 0
+
+    def test_interior_tiles_random_has_none(self):
+        from paper_2510_13536_b200.dist import interior_tiles, local_rows, partition
+        A = _gen(8192)
+        part = partition(A.n_rows, 2)
+        lo, hi = part.rows(1)
+        ilo, ihi = interior_tiles(local_rows(A, lo, hi), lo, hi)
+        assert ihi == ilo
+
+    def test_tile_column_ranges_empty_rows(self):
+        from paper_2510_13536_b200.dist import tile_column_ranges
+        A = CsrMatrix(1500, 1500, np.r_[np.zeros(1025, np.int64), np.arange(1, 477)],
+                      np.arange(1024, 1500), np.ones(476))     # rows 0..1023 empty
+        mn, mx = tile_column_ranges(A)
+        assert list(mn) == [1500, 1024] and list(mx) == [-1, 1499]

@@ -1,0 +1,4 @@
+set -x
+python tools/k1w_sweep.py --config C2 --variants 'MWCG_K1W=0;MWCG_K1W=1;MWCG_K1W=1,MWCG_K1W_VS=0' --out gpurun_out/r2f_sweep_c2.json > gpurun_out/r2f_sweep.log 2>&1
+python tools/k1w_sweep.py --config C4 --modes dw,qtw --variants 'MWCG_K1W=0;MWCG_K1W=1' --out gpurun_out/r2f_sweep_c4.json >> gpurun_out/r2f_sweep.log 2>&1
+python -m pytest tests/test_gpu_k1w.py -x -q -k "default or every" > gpurun_out/r2f_k1w.log 2>&1; tail -3 gpurun_out/r2f_k1w.log
