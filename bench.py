@@ -57,6 +57,8 @@ def parse():
                     help="comma list of other BASELINE configs to time per arithmetic and "
                          "report under 'configs' (not part of value); '' for none")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-stock", action="store_true",
+                    help="--impl reference: skip timing the stock Python/numba reference")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--partitioned", action="store_true",
                     help="force the row-partitioned NCCL path (also at N=1 under torchrun)")
@@ -182,6 +184,45 @@ def cpu_sample(cfg, mode, seconds, threads):
 
 
 # ---------------------------------------------------------------------------
+def base_config(cfg, mode):
+    """The `config` dict of BOTH arms (same workload, same keys)."""
+    A = cfg["A"]
+    w = WORDS[mode]
+    return {"workload": workload_name(cfg, mode), "mode": mode, "n": int(A.n_rows), "nnz": int(A.nnz),
+            "epsilon": cfg["epsilon"],
+            "l2": f"inputs larger than L2 (A {12 * A.nnz / 1e6:.0f} MB + vectors "
+                  f"{4 * 8 * w * A.n_rows / 1e6:.0f} MB > 126 MB)"}
+
+
+def stock_reference(budget_s=150.0):
+    """The UNMODIFIED reference package (Python + numba, baseline/_ref) through
+    its public cg_solve on ONE host core (it is single-threaded): C1 full
+    solves (TW: a 30-iteration sample, its full solve takes ~100 s) and a
+    10-iteration C2 DW sample.  Each run is a subprocess
+    (oracle/stock_reference.py) pinned to one core; JIT warm-up untimed."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import stock_reference as sr
+    if not sr.available():
+        return {"unavailable": "baseline/_ref not installed (pip install --target baseline/_ref "
+                               "/root/reference/pkg)"}
+    runs = [("C1", m, 0) for m in ("fp64", "dw", "qdw", "qtw")] + [("C1", "tw", 30), ("C2", "dw", 10)]
+    out, t0 = [], time.perf_counter()
+    for cfg, mode, iters in runs:
+        left = budget_s - (time.perf_counter() - t0)
+        if left < 10:
+            out.append({"config": cfg, "mode": mode, "skipped": "time budget"})
+            continue
+        cmd = [sys.executable, os.path.join(ROOT, "oracle", "stock_reference.py"), "--config", cfg,
+               "--mode", mode] + (["--iters", str(iters)] if iters else [])
+        try:
+            pr = subprocess.run(cmd, capture_output=True, text=True, timeout=left)
+            out.append(json.loads(pr.stdout.strip().splitlines()[-1]))
+        except Exception as exc:  # pragma: no cover - reported, never fatal
+            out.append({"config": cfg, "mode": mode, "error": f"{type(exc).__name__}: {exc}"[:200]})
+    return {"runs": out, "cores": 1,
+            "note": "stock mwcg 0.1.0 (reference package, Python + numba, single-threaded by design)"}
+
+
 def run_reference(a):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -199,18 +240,23 @@ def run_reference(a):
         tot_it += it
         tot_t += dt
     v = tot_it / tot_t
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import stock_reference as sr
     line = {
         "impl": "reference", "metric": "CG iterations/s", "value": v, "unit": "iter/s",
         "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": 1e3 * tot_t / a.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload_name(cfg, a.mode), "mode": a.mode,
-                   "parallelism": f"{threads} host threads"},
+        "config": base_config(cfg, a.mode),
         "cpu_baseline": {"value": v, "unit": "iter/s", "cores": threads, "kind": "port",
+                         "cpu_model": sr.cpu_model(),
                          "sample": f"{tot_it} unconditional CG iterations of {cfg['name']} in "
-                                   f"{a.mode} (oracle/mwcg_oracle.c, partitions={threads})"},
+                                   f"{a.mode} (oracle/mwcg_oracle.c: the reference algorithm in C, "
+                                   f"OpenMP over rows, partitions={threads} dot shape)"},
         "e2e": {"value": v, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if not a.no_stock:
+        line["stock_reference"] = stock_reference()
     print(json.dumps(line), flush=True)
     return 0
 
@@ -514,13 +560,12 @@ def run_ours(a):
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload_name(cfg, mode), "mode": mode, "n": n, "nnz": nnz,
-                       "epsilon": eps, "iterations_per_solve": iters_per_solve,
-                       "reason": reason, "time_to_solution_s": ms_per_step * 1e-3,
-                       "parallelism": "replicas" if world > 1 else "single",
-                       "l2": f"inputs larger than L2 (A {12 * nnz / 1e6:.0f} MB + vectors "
-                             f"{4 * 8 * w * n / 1e6:.0f} MB > 126 MB)",
-                       "reduction": "canonical tile tree (bitwise-reproducible)"},
+            "config": base_config(cfg, mode),
+            "solve": {"iterations_per_solve": iters_per_solve, "reason": reason,
+                      "time_to_solution_s": ms_per_step * 1e-3,
+                      "parallelism": "replicas" if world > 1 else "single",
+                      "reduction": "canonical tile tree (bitwise-reproducible)",
+                      "kernels": solver.describe()},
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -95,11 +95,18 @@ int mwcg_matrix_create(mwcg_matrix **out, int64_t n_rows, int64_t n_cols, int64_
  * column offsets when the 32 rows of each slice share them -- stencils, bands
  * -- else int16 column deltas when every |col - row| < 2^15, else int32),
  * 0 int32, 1 int16, 2 slice-shared offsets (error if a slice needs more than
- * its longest row + 2 slots). */
+ * its longest row + 2 slots).  The SELL layouts (0, 1, auto) sort the rows of
+ * each 1024-row tile by length (SELL-sigma, sigma = 1024) when that cuts the
+ * slice padding by >= 5 %; OR-ing MWCG_SELL_SIGMA forces the sort,
+ * MWCG_SELL_NO_SIGMA disables it (with a flag, "auto" is written 15).  Row
+ * results are unchanged (each row is still summed left to right). */
+#define MWCG_SELL_SIGMA 16
+#define MWCG_SELL_NO_SIGMA 32
 int mwcg_matrix_create_ex(mwcg_matrix **out, int64_t n_rows, int64_t n_cols, int64_t nnz,
                           const void *row_ptr, const void *col_idx, const double *values,
                           int index_bytes, int64_t row_base, int col_format, void *stream);
 int mwcg_matrix_col_bytes(const mwcg_matrix *A);   /* 2 (int16 deltas), 4 (int32), 0 (slice-shared) */
+int mwcg_matrix_sigma_sorted(const mwcg_matrix *A); /* 1 if the rows of each tile are length-sorted */
 int mwcg_matrix_destroy(mwcg_matrix *A);
 int mwcg_matrix_info(const mwcg_matrix *A, int64_t *n_rows, int64_t *n_cols, int64_t *nnz,
                      int64_t *padded_entries);
@@ -154,9 +161,8 @@ int mwcg_solver_run_profiled(mwcg_solver *s, int64_t k_stop, double *ms);
 int mwcg_solver_time_k1(mwcg_solver *s, int reps, double *us);
 int mwcg_solver_state(mwcg_solver *s, mwcg_state *out);
 /* Kernel configuration the solver chose (introspection for tests / bench):
- * out[0] windowed K1 in use (0/1), [1] its values staged in the ring (0/1), [2] ring slots (tiles),
- * [3] p windows per stage, [4..7] grid of K1 / K2 / K3 / init,
- * [8] TMA-staged K2, [9] TMA-staged K3.  n: capacity of out. */
+ * out[0..3] grid of K1 / K2 / K3 / init, [4] TMA-staged K2, [5] TMA-staged
+ * K3, [6] SELL-sigma row order.  n: capacity of out. */
 int mwcg_solver_describe(const mwcg_solver *s, int64_t *out, int n);
 /* norm_metrics_tw (kernels.py:305-328) of the current iterate */
 int mwcg_solver_metrics(mwcg_solver *s, double *err, double *true_res);

@@ -18,6 +18,7 @@ STATUS = {0: "running", 1: "converged", 2: "max_iterations", 3: "breakdown"}
 STAGE = {"init": 0, "final_init": 1, "spmv": 2, "final_alpha": 3, "update": 4, "final_beta": 5,
          "xpay": 6, "spmv_interior": 7, "spmv_boundary": 8}
 ERR_VALUE = 1001
+SELL_SIGMA, SELL_NO_SIGMA = 16, 32  # col_format flags (include/mwcg_cuda.h)
 
 c_i64 = ctypes.c_int64
 c_dp = ctypes.POINTER(ctypes.c_double)
@@ -100,6 +101,7 @@ SIGNATURES = {
                                                c_i64, c_vp, c_i64, c_i64, c_i64, c_vp]),
     "mwcg_solver_dist_stage": (ctypes.c_int, [c_vp, ctypes.c_int, c_vp]),
     "mwcg_solver_set_interior": (ctypes.c_int, [c_vp, c_i64, c_i64]),
+    "mwcg_matrix_sigma_sorted": (ctypes.c_int, [c_vp]),
 }
 
 _lib = None

@@ -214,8 +214,10 @@ __global__ void __launch_bounds__(SpTraits<M>::THREADS, SpTraits<M>::MINB)
     constexpr int RPT = SpTraits<M>::RPT;
     // 256 threads: thread t owns rows t + 256 j, which IS the canonical tile
     // mapping, so its p.q terms accumulate in registers in canonical order;
-    // 512 threads (FP64) stage the terms in shared memory for the first 256
-    constexpr bool STAGE = FUSED && NT != TILE_THREADS;
+    // 512 threads (FP64) and the SELL layouts (whose rows may be sorted by
+    // length inside the tile: SELL-sigma) stage the terms in shared memory by
+    // natural row, and the first 256 threads replay the canonical order
+    constexpr bool STAGE = FUSED && (NT != TILE_THREADS || !std::is_same<CT, DiaTag>::value);
     __shared__ double terms[STAGE ? W * TILE : 1];
     __shared__ double smem[W * TILE_THREADS / 32];
     __shared__ int s_last;
@@ -232,14 +234,15 @@ __global__ void __launch_bounds__(SpTraits<M>::THREADS, SpTraits<M>::MINB)
         V<W> acc = zero<W>();
 #pragma unroll 1
         for (int k = 0; k < RPT; k++) {
-            const int li = threadIdx.x + k * NT;  // row inside the tile
-            const int64_t row = tile * TILE + li;
+            const int lp = threadIdx.x + k * NT;  // storage position inside the tile
+            const int64_t pos = tile * TILE + lp;
             const SliceWords sw = nsw;
-            if (k + 1 < RPT) nsw = slice_words(A, row + NT);
+            if (k + 1 < RPT) nsw = slice_words(A, pos + NT);
             V<W> term = zero<W>();
-            if (row < n) {
+            const int64_t row = std::is_same<CT, DiaTag>::value ? pos : sell_row(A, pos);
+            if (pos < n) {
                 // columns are global: p is the full (replicated) vector
-                V<W> sv = spmv_row<M, SpTraits<M>::U, CT, true>(A, p, 0, row, sw);
+                V<W> sv = spmv_row<M, SpTraits<M>::U, CT, true>(A, p, 0, pos, sw);
                 if (norm_all) sv = Ar::norm(sv);
                 store<W>(q, g.ld, row, sv);
                 if (FUSED) term = Ar::mul(load_aos_ro<W>(p, g.p_off + row), sv);
@@ -247,7 +250,7 @@ __global__ void __launch_bounds__(SpTraits<M>::THREADS, SpTraits<M>::MINB)
             }
             if (STAGE) {
 #pragma unroll
-                for (int w = 0; w < W; w++) terms[w * TILE + li] = term.w[w];
+                for (int w = 0; w < W; w++) terms[w * TILE + (row - tile * TILE)] = term.w[w];
             }
         }
         if (STAGE) {
@@ -268,231 +271,6 @@ __global__ void __launch_bounds__(SpTraits<M>::THREADS, SpTraits<M>::MINB)
         if (FUSED) {
             acc = block_tree_first<M, TILE_THREADS>(acc, smem);
             if (threadIdx.x == 0) store_part<W>(part, g.part_ld, g.tile_off + tile, acc);
-        }
-    }
-    if (!FUSED || !g.final_) return;
-    if (!last_block_done(&st->ticket[0], &s_last)) return;
-    V<W> pq = reduce_partials_first<M>(part, g.part_ld, g.ntiles_glob, smem);
-    if (threadIdx.x == 0) {
-        st->ticket[0] = 0u;
-        scalar_alpha<M>(st, pq, h, use_cond);
-    }
-}
-
-// ---------------------------------------------------------------- K1W
-// Windowed K1 for the slice-shared-offset layout (stencils, bands: C1-C4).
-// The tile's rows are processed in stages of R rows (R = 256, 512 or 1024).
-// A producer warp brings everything a stage reads into a shared-memory ring
-// with 1-D bulk copies (cp.async.bulk, mbarrier per stage):
-//   * the stage's slice descriptors and its matrix values (contiguous),
-//   * the windows of p the stage gathers from: the distinct column offsets
-//     of the matrix, clustered (offsets closer than R + 4 share a cluster),
-//     give one contiguous window per cluster, [g0 + omin_j, g0 + R - 1 +
-//     omax_j] for a stage starting at global row g0.
-// The consumer threads (256 or 512) then walk their rows with every operand in shared
-// memory: a row's dependency chain is the L1-resident slot word -> a shared
-// load -> the FP64 chain, instead of descriptor (L2) -> pattern (L1) ->
-// gather of p (L2) with HBM values in between (round 1: K1 was latency-bound
-// on that chain, DESIGN.md §3 item 1).  The p.q terms are reduced in the
-// canonical tile order and each row's left-to-right sum is unchanged --
-// results are bitwise K1's.
-constexpr int K1W_MAXCLU = 16;
-constexpr int K1W_MAXNS = 8;
-
-struct WinPlan {
-    int NS, nclu, vs;                // ring slots (whole tiles), p windows, values staged
-    int stage_doubles;               // one ring stage
-    int val_off, win_off, desc_off;  // section offsets (doubles) in a stage
-    int sd0;                         // shared index delta of the diagonal record
-    int omin[K1W_MAXCLU], pre[K1W_MAXCLU], span[K1W_MAXCLU];
-    const uint2 *tab;                // per pattern slot: {lane mask, shared index delta}
-};
-
-// named barriers of K1W (0 is __syncthreads)
-__device__ __forceinline__ void named_bar(int id, int nthreads) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
-
-// block tree over the first NT threads, synchronised with named barrier 1
-// (the producer warp and any further consumers do not take part)
-template <int M, int NT>
-__device__ __forceinline__ V<Arith<M>::W> block_tree_bar(V<Arith<M>::W> v, double *smem) {
-    using Ar = Arith<M>;
-    constexpr int W = Ar::W;
-    constexpr int NW = NT / 32;
-    v = warp_tree<M>(v);
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    if (lane == 0) {
-#pragma unroll
-        for (int k = 0; k < W; k++) smem[k * NW + wid] = v.w[k];
-    }
-    named_bar(1, NT);
-    if (wid == 0) {
-        V<W> u = zero<W>();
-        if (lane < NW) {
-#pragma unroll
-            for (int k = 0; k < W; k++) u.w[k] = smem[k * NW + lane];
-        }
-#pragma unroll
-        for (int off = NW / 2; off >= 1; off >>= 1) u = Ar::add(u, shfl_down<W>(u, off));
-        v = u;
-    }
-    named_bar(1, NT);
-    return v;
-}
-
-template <int W>
-__device__ __forceinline__ V<W> ld_rec(const double *base, int idx) {
-    V<W> r;
-    if (W == 2) {
-        const double2 t = *reinterpret_cast<const double2 *>(base + 2 * idx);
-        r.w[0] = t.x;
-        r.w[W - 1] = t.y;
-    } else {
-#pragma unroll
-        for (int k = 0; k < W; k++) r.w[k] = base[W * idx + k];
-    }
-    return r;
-}
-
-// One thread per row of the tile: 1024 threads (32 warps), row c of every
-// tile the CTA walks is thread c's.  A ring of NS whole-tile slots; thread 0
-// refills a slot with the CTA's tile NS ahead once every thread is done with
-// it (two CTA barriers per tile), so NS - 1 tiles of operands are in flight
-// while one is computed.  A slot holds the tile's slice descriptors, the p
-// windows and -- when they fit (VS: values staged; stencils with few slots)
-// -- the tile's matrix values; otherwise the values stream straight from HBM
-// (ld.global.cs, all U loads of a chunk in flight per thread).  The p.q
-// terms are replayed by the first 256 threads in the canonical order from
-// the q just written (global, this CTA's own stores) and p (the window).
-constexpr int K1W_THREADS = TILE;
-
-template <int M, bool VS>
-struct K1wTraits {
-    static constexpr int U = VS ? 4 : 8;
-};
-
-template <int M, bool FUSED, bool VS>
-__global__ void __launch_bounds__(K1W_THREADS, 1)
-    cg_spmv_pq_win(SellMatrix A, const double *__restrict__ p, double *__restrict__ q, Geo g,
-                   double *__restrict__ part, CgState *st, WinPlan wp, cudaGraphConditionalHandle h,
-                   int use_cond) {
-    using Ar = Arith<M>;
-    constexpr int W = Ar::W;
-    constexpr int U = K1wTraits<M, VS>::U;
-    constexpr uint64_t LO = (1ull << 36) - 1;
-    extern __shared__ __align__(128) double ring[];
-    __shared__ uint64_t full[K1W_MAXNS];
-    __shared__ double smem[W * TILE_THREADS / 32];
-    __shared__ int s_last;
-    if (stopped_k1(st, h, use_cond)) return;
-    const bool norm_all = st->norm_all != 0;
-    const int64_t n = g.n;
-    const int dir = (int)(st->k & 1);
-    const int NS = wp.NS;
-    const int64_t cnt = k1_count(g);
-    const int64_t nmine = cnt > blockIdx.x ? (cnt - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-    const int c = threadIdx.x, lane = c & 31;
-    const int64_t ldp_even = (g.ldp + 1) & ~(int64_t)1;
-    constexpr int ND = TILE / SLICE + 2;  // descriptors per slot (even count)
-    // slot refill (thread 0): descriptors, [values], p windows of tile tix
-    auto issue = [&](int64_t tix) {
-        const int sidx = (int)(tix % NS);
-        double *stg = ring + (size_t)sidx * wp.stage_doubles;
-        const int64_t tile = k1_tile(g, snake(blockIdx.x + tix * gridDim.x, cnt, dir));
-        const int64_t r0 = tile * TILE;
-        const int64_t sl0 = r0 >> 5;
-        const int64_t sl1 = min(sl0 + TILE / SLICE, A.n_slices);
-        const int64_t v0 = (int64_t)(__ldg((const unsigned long long *)A.slice_ptr + sl0) & LO) << 5;
-        const int64_t v1 = (int64_t)(__ldg((const unsigned long long *)A.slice_ptr + sl1) & LO) << 5;
-        const int64_t g0 = A.row_base + r0;
-        // window j: global records [lo, hi) clipped to [0, ldp), widened to
-        // even records (16-B aligned copies; pre[j] keeps the shared
-        // position's parity equal to the global one)
-        auto win = [&](int j, int64_t &lo, int64_t &clo, int64_t &chi) {
-            lo = g0 + wp.omin[j];
-            const int64_t hi = g0 + TILE + wp.omin[j] + wp.span[j];
-            clo = max(lo, (int64_t)0) & ~(int64_t)1;
-            chi = min((min(hi, g.ldp) + 1) & ~(int64_t)1, ldp_even);
-        };
-        uint32_t bytes = (uint32_t)(ND * 8) + (VS ? (uint32_t)((v1 - v0) * 8) : 0u);
-        for (int j = 0; j < wp.nclu; j++) {
-            int64_t lo, clo, chi;
-            win(j, lo, clo, chi);
-            if (chi > clo) bytes += (uint32_t)((chi - clo) * 8 * W);
-        }
-        const uint64_t pol_stream = l2_policy_evict_first(), pol_keep = l2_policy_evict_last();
-        mbar_arrive_expect_tx(&full[sidx], bytes);
-        bulk_g2s(stg + wp.desc_off, A.slice_ptr + sl0, (uint32_t)(ND * 8), &full[sidx]);
-        if (VS && v1 > v0)
-            bulk_g2s_hint(stg + wp.val_off, A.vals + v0, (uint32_t)((v1 - v0) * 8), &full[sidx], pol_stream);
-        for (int j = 0; j < wp.nclu; j++) {
-            int64_t lo, clo, chi;
-            win(j, lo, clo, chi);
-            if (chi > clo)
-                bulk_g2s_hint(stg + wp.win_off + (int64_t)(j * TILE + wp.pre[j] + (clo - lo)) * W, p + clo * W,
-                              (uint32_t)((chi - clo) * 8 * W), &full[sidx], pol_keep);
-        }
-    };
-    if (c == 0) {
-        for (int i = 0; i < NS; i++) mbar_init(&full[i], 1);
-        mbar_init_fence();
-        for (int64_t i = 0; i < NS && i < nmine; i++) issue(i);
-    }
-    __syncthreads();
-    for (int64_t tix = 0; tix < nmine; tix++) {
-        const int sidx = (int)(tix % NS);
-        const int64_t tile = k1_tile(g, snake(blockIdx.x + tix * gridDim.x, cnt, dir));
-        const int64_t row = tile * TILE + c;
-        mbar_wait(&full[sidx], (uint32_t)((tix / NS) & 1));
-        const double *stg = ring + (size_t)sidx * wp.stage_doubles;
-        const double *sw = stg + wp.win_off;
-        if (row < n) {
-            const uint64_t *dsc = reinterpret_cast<const uint64_t *>(stg + wp.desc_off);
-            const uint64_t d0 = dsc[c >> 5], d1 = dsc[(c >> 5) + 1];
-            const int L = (int)((d1 & LO) - (d0 & LO));
-            const uint2 *tp = wp.tab + (d0 >> 36);
-            const double *vp = VS ? stg + wp.val_off + (((d0 & LO) - (dsc[0] & LO)) << 5) + lane
-                                  : A.vals + ((int64_t)(d0 & LO) << 5) + lane;
-            V<W> sacc = zero<W>();
-            for (int k0 = 0; k0 < L; k0 += U, tp += U, vp += U * SLICE) {
-                uint2 tw[U];
-                double a[U];
-#pragma unroll
-                for (int u = 0; u < U; u++) {
-                    tw[u] = __ldg(tp + u);
-                    a[u] = VS ? vp[u * SLICE] : ld_stream(vp + u * SLICE);  // (padded past the end)
-                }
-                bool ok[U];
-                V<W> xv[U];
-#pragma unroll
-                for (int u = 0; u < U; u++) {
-                    ok[u] = (tw[u].x >> lane) & 1u;
-                    xv[u] = ld_rec<W>(sw, c + (ok[u] ? (int)tw[u].y : wp.sd0));
-                }
-#pragma unroll
-                for (int u = 0; u < U; u++)
-                    if (ok[u]) sacc = Ar::add(sacc, Ar::dxmul(a[u], xv[u]));
-            }
-            if (norm_all) sacc = Ar::norm(sacc);
-            store<W>(q, g.ld, row, sacc);
-        }
-        __syncthreads();  // q of the whole tile is written (and visible to the CTA)
-        if (FUSED && c < TILE_THREADS) {
-            V<W> acc = zero<W>();
-#pragma unroll
-            for (int j = 0; j < TILE_ELEMS; j++) {
-                const int cc = c + j * TILE_THREADS;
-                const int64_t rr = tile * TILE + cc;
-                if (rr < n) acc = Ar::add(acc, Ar::mul(ld_rec<W>(sw, cc + wp.sd0), load<W>(q, g.ld, rr)));
-            }
-            const V<W> tot = block_tree_bar<M, TILE_THREADS>(acc, smem);
-            if (c == 0) store_part<W>(part, g.part_ld, g.tile_off + tile, tot);
-        }
-        __syncthreads();  // slot sidx is free
-        if (c == 0 && tix + NS < nmine) {
-            fence_proxy_async_smem();
-            issue(tix + NS);
         }
     }
     if (!FUSED || !g.final_) return;
@@ -959,9 +737,9 @@ template <int M, typename CT>
 __global__ void __launch_bounds__(TILE_THREADS)
     spmv_aos_kernel(SellMatrix A, const double *__restrict__ p, double *__restrict__ q, int64_t ldq) {
     constexpr int W = Arith<M>::W;
-    for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < A.n_rows;
-         row += (int64_t)gridDim.x * blockDim.x)
-        store<W>(q, ldq, row, spmv_row<M, 8, CT, true>(A, p, 0, row));
+    for (int64_t pos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; pos < A.n_rows;
+         pos += (int64_t)gridDim.x * blockDim.x)
+        store<W>(q, ldq, sell_row(A, pos), spmv_row<M, 8, CT, true>(A, p, 0, pos));
 }
 
 // ---------------------------------------------------------------- finalize (multi-rank)
@@ -1052,8 +830,9 @@ __global__ void __launch_bounds__(TILE_THREADS)
     const int64_t n = A.n_rows;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = sell_row(A, i);  // i: storage position of a row
         V<3> qi = spmv_row<TW, 8, CT>(A, xt, n, i);
-        store<3>(res, n, i, dxtw_add(b[i], neg<3>(qi)));
+        store<3>(res, n, r, dxtw_add(b[r], neg<3>(qi)));
         if (xs) store<3>(diff, n, i, dxtw_add(xs[i], neg<3>(load<3>(xt, n, i))));
     }
 }
@@ -1101,12 +880,7 @@ struct mwcg_solver {
     bool tma = false;                    // TMA-staged K3 (aligned planes; MWCG_TMA=0/1 overrides)
     bool tma2 = false;                   // TMA-staged K2 (MWCG_TMA2=0/1 overrides)
     cudaAccessPolicyWindow l2win{};      // K1's persisting-L2 window over p (num_bytes 0: none)
-    const SellMatrixOwned *Mown = nullptr;
     int64_t ilo = 0, ihi = 0;            // interior tiles of a rank (SPMV_INTERIOR)
-    bool k1w = false;                    // windowed K1 (dia layout; MWCG_K1W=0/1 overrides)
-    WinPlan wp{};
-    size_t k1w_smem = 0;
-    uint2 *wtab = nullptr;               // K1W slot table (device)
 };
 
 namespace {
@@ -1133,17 +907,6 @@ void launch_k1(mwcg_solver *s, cudaStream_t st, cudaGraphConditionalHandle h, in
     cfg.attrs = at;
     cfg.numAttrs = s->l2win.num_bytes > 0 ? 1 : 0;
     const double *pc = s->p;
-    if (s->k1w) {
-        cfg.blockDim = dim3(K1W_THREADS);
-        cfg.dynamicSmemBytes = s->k1w_smem;
-        if (s->wp.vs)
-            cudaLaunchKernelEx(&cfg, cg_spmv_pq_win<M, FUSED, true>, s->A, pc, s->q, g, s->part, s->st, s->wp, h,
-                               use_cond);
-        else
-            cudaLaunchKernelEx(&cfg, cg_spmv_pq_win<M, FUSED, false>, s->A, pc, s->q, g, s->part, s->st, s->wp, h,
-                               use_cond);
-        return;
-    }
 #define K1_LAUNCH(CT) \
     cudaLaunchKernelEx(&cfg, cg_spmv_pq<M, FUSED, CT>, s->A, pc, s->q, g, s->part, s->st, h, use_cond)
     if (s->A.dia) K1_LAUNCH(DiaTag);
@@ -1275,90 +1038,6 @@ int enqueue_dist_stage(mwcg_solver *s, int stage) {
     return 0;
 }
 
-// Plan the windowed K1 (cg_spmv_pq_win) for a dia-layout matrix: cluster
-// the distinct column offsets (offsets closer than a tile share a window),
-// size one whole-tile ring slot (descriptors + windows [+ values]), and take
-// the values into the slot when >= 2 such slots fit `budget` (else they
-// stream from HBM and only windows are staged, >= 2 slots).  Builds the
-// per-slot table {lane mask, shared index delta}.  Returns false when no
-// ring fits (the classic K1 is used).  MWCG_K1W_VS=0/1 forces the variant.
-bool plan_windows(mwcg_solver *s, int W, size_t budget) {
-    const SellMatrixOwned *M = s->Mown;
-    if (!M || !s->A.dia || M->pat_host.empty() || (s->A.row_base & 1)) return false;
-    const std::vector<uint64_t> &pat = M->pat_host;
-    std::vector<int> offs{0};
-    for (uint64_t w : pat)
-        if (w >> 32) offs.push_back((int)(uint32_t)w);
-    std::sort(offs.begin(), offs.end());
-    offs.erase(std::unique(offs.begin(), offs.end()), offs.end());
-    const int64_t ns = s->A.n_slices;
-    auto align16 = [](int64_t d) { return (d + 15) & ~(int64_t)15; };  // doubles -> 128 B
-    WinPlan wp{};
-    std::vector<int> omin, omax;
-    for (int o : offs) {
-        if (omin.empty() || (int64_t)o - omax.back() > TILE + 4) {
-            omin.push_back(o);
-            omax.push_back(o);
-        } else {
-            omax.back() = o;
-        }
-    }
-    if ((int)omin.size() > K1W_MAXCLU) return false;
-    wp.nclu = (int)omin.size();
-    int64_t pre = 1;
-    for (int j = 0; j < wp.nclu; j++) {
-        if (((pre - omin[j]) % 2 + 2) % 2) pre++;  // window j copies start 16-B aligned
-        wp.omin[j] = omin[j];
-        wp.span[j] = omax[j] - omin[j];
-        wp.pre[j] = (int)pre;
-        pre += wp.span[j] + 4;
-    }
-    const int64_t win_recs = (int64_t)wp.nclu * TILE + pre;
-    int64_t vslots = 0;  // most value slots any tile holds
-    for (int64_t sl = 0; sl < ns; sl += TILE / SLICE) {
-        const int64_t e = std::min<int64_t>(sl + TILE / SLICE, ns);
-        vslots = std::max<int64_t>(vslots, (int64_t)((M->desc_host[e] & ((1ull << 36) - 1)) -
-                                                     (M->desc_host[sl] & ((1ull << 36) - 1))));
-    }
-    const char *fv = std::getenv("MWCG_K1W_VS");
-    for (int vs : {1, 0}) {
-        if (fv && std::atoi(fv) != vs) continue;
-        wp.vs = vs;
-        wp.val_off = 0;
-        wp.win_off = vs ? (int)align16(vslots * SLICE + 8 * SLICE) : 0;  // + slack: chunks read past a slice
-        wp.desc_off = (int)(wp.win_off + align16(win_recs * W));
-        wp.stage_doubles = (int)(wp.desc_off + align16(TILE / SLICE + 2));
-        const size_t slot_bytes = sizeof(double) * (size_t)wp.stage_doubles;
-        const int NS = (int)std::min<size_t>(K1W_MAXNS, budget / slot_bytes);
-        if (NS < 2) continue;
-        wp.NS = NS;
-        // shared index delta of every pattern slot (row c reads record c + delta)
-        auto delta = [&](int off) {
-            int j = 0;
-            while (j + 1 < wp.nclu && off > omax[j]) j++;
-            return j * TILE + wp.pre[j] + (off - wp.omin[j]);
-        };
-        wp.sd0 = delta(0);
-        std::vector<uint2> tab(pat.size());
-        for (size_t k = 0; k < pat.size(); k++) {
-            const uint32_t mask = (uint32_t)(pat[k] >> 32);
-            tab[k] = make_uint2(mask, (unsigned)(mask ? delta((int)(uint32_t)pat[k]) : wp.sd0));
-        }
-        if (s->wtab) pool_free(s->wtab, s->stream);
-        s->wtab = nullptr;
-        if (pool_alloc((void **)&s->wtab, sizeof(uint2) * tab.size(), s->stream) != cudaSuccess) return false;
-        if (cudaMemcpyAsync(s->wtab, tab.data(), sizeof(uint2) * tab.size(), cudaMemcpyHostToDevice,
-                            s->stream) != cudaSuccess ||
-            cudaStreamSynchronize(s->stream) != cudaSuccess)
-            return false;
-        wp.tab = s->wtab;
-        s->wp = wp;
-        s->k1w_smem = slot_bytes * (size_t)NS;
-        return true;
-    }
-    return false;
-}
-
 template <int M>
 int compute_grids_t(mwcg_solver *s) {
     int dev = 0, sms = 0;
@@ -1411,29 +1090,6 @@ int compute_grids_t(mwcg_solver *s) {
         const char *t2 = std::getenv("MWCG_TMA2");
         s->tma2 = t2 ? t2[0] != '0' : (M != FP64 && M != TW);
     }
-    {
-        // windowed K1 for the slice-shared-offset layout (MWCG_K1W=0/1 overrides)
-        const char *t = std::getenv("MWCG_K1W");
-        s->k1w = false;
-        if (!t || t[0] != '0') {
-            int maxsm = 0;
-            cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-            // dynamic budget: the opt-in maximum less the static shared memory
-            const size_t budget = (size_t)std::max(0, maxsm - 1024);
-            s->k1w = plan_windows(s, Arith<M>::W, budget);
-            if (s->k1w) {
-                // the attribute is per function (shared by every solver of this
-                // mode): always the full budget, never one solver's ring size
-                const int dyn = (int)budget;
-                cudaFuncSetAttribute(cg_spmv_pq_win<M, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
-                cudaFuncSetAttribute(cg_spmv_pq_win<M, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
-                cudaFuncSetAttribute(cg_spmv_pq_win<M, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
-                cudaFuncSetAttribute(cg_spmv_pq_win<M, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
-                if (cudaGetLastError() != cudaSuccess) s->k1w = false;
-            }
-        }
-        cudaGetLastError();
-    }
     if (s->fused) {
         MWCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb[0], cg_spmv_pq<M, true, int32_t>,
                                                                 SpTraits<M>::THREADS, 0));
@@ -1475,10 +1131,6 @@ int compute_grids_t(mwcg_solver *s) {
     // slower for the streaming ones; MWCG_GRID_FULL=<mask> overrides
     unsigned full = (M == TW) ? 7u : ((M == QTW) ? 1u : 0u);
     if (const char *t = std::getenv("MWCG_GRID_FULL")) full = (unsigned)std::atoi(t);
-    if (s->k1w) {
-        nb[0] = 1;             // one CTA (ring) per SM, persistent
-        full &= ~1u;
-    }
     for (int i = 0; i < 4; i++) {
         int64_t g = (int64_t)(nb[i] > 0 ? nb[i] : 1) * sms;
         if (g > s->geo.ntiles || ((full >> i) & 1u)) g = s->geo.ntiles;
@@ -1543,7 +1195,6 @@ void free_solver(mwcg_solver *s) {
     pool_free(s->mpart, st);
     pool_free(s->mout, st);
     pool_free(s->mticket, st);
-    pool_free(s->wtab, st);
     delete[] reinterpret_cast<double *>(s->st_host);
     for (auto &e : s->ev)
         if (e) cudaEventDestroy(e);
@@ -1586,6 +1237,8 @@ int mwcg_matrix_create_ex(mwcg_matrix **out, int64_t n_rows, int64_t n_cols, int
     *out = new mwcg_matrix{M};
     return 0;
 }
+
+int mwcg_matrix_sigma_sorted(const mwcg_matrix *A) { return A && A->M->view.perm ? 1 : 0; }
 
 int mwcg_matrix_col_bytes(const mwcg_matrix *A) {
     return A ? (A->M->view.dia ? 0 : (A->M->view.col16 ? 2 : 4)) : -1;
@@ -1641,7 +1294,6 @@ int mwcg_solver_create(mwcg_solver **out, const mwcg_matrix *A, const mwcg_solve
     }
     auto *s = new mwcg_solver();
     s->A = A->M->view;
-    s->Mown = A->M;
     s->mode = cfg->mode;
     s->W = words_of(cfg->mode);
     s->cfg = *cfg;
@@ -1670,8 +1322,7 @@ int mwcg_solver_create(mwcg_solver **out, const mwcg_matrix *A, const mwcg_solve
         s->own_x = true;
     }
     TRY(pool_alloc((void **)&s->r, vbytes, s->stream));
-    // p: one spare record (K1W's window copies end on an even record)
-    TRY(pool_alloc((void **)&s->p, vbytes + sizeof(double) * (size_t)s->W, s->stream));
+    TRY(pool_alloc((void **)&s->p, vbytes, s->stream));
     TRY(pool_alloc((void **)&s->q, vbytes, s->stream));
     int64_t np = s->fused ? (s->ntiles > 0 ? s->ntiles : 1) : s->parts;
     TRY(pool_alloc((void **)&s->part, sizeof(double) * 3 * (size_t)np, s->stream));
@@ -1727,7 +1378,6 @@ int mwcg_solver_create_dist(mwcg_solver **out, const mwcg_matrix *A, const mwcg_
     }
     auto *s = new mwcg_solver();
     s->A = A->M->view;
-    s->Mown = A->M;
     s->mode = cfg->mode;
     s->W = words_of(cfg->mode);
     s->cfg = *cfg;
@@ -1823,9 +1473,9 @@ int mwcg_solver_describe(const mwcg_solver *s, int64_t *out, int n) {
         set_error("null argument");
         return MWCG_ERR_VALUE;
     }
-    const int64_t v[10] = {s->k1w ? 1 : 0, s->k1w ? s->wp.vs : 0, s->k1w ? s->wp.NS : 0, s->k1w ? s->wp.nclu : 0,
-                           s->grid[0], s->grid[1], s->grid[2], s->grid[3], s->tma2 ? 1 : 0, s->tma ? 1 : 0};
-    for (int i = 0; i < n && i < 10; i++) out[i] = v[i];
+    const int64_t v[7] = {s->grid[0], s->grid[1], s->grid[2], s->grid[3], s->tma2 ? 1 : 0, s->tma ? 1 : 0,
+                          s->A.perm ? 1 : 0};
+    for (int i = 0; i < n && i < 7; i++) out[i] = v[i];
     return 0;
 }
 

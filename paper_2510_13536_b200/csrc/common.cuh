@@ -58,7 +58,15 @@ struct SellMatrix {
     const double *vals;
     const uint64_t *om;     // dia: pattern table of slot words (lane mask << 32 | uint32 offset);
                             // slice_ptr then holds descriptors (start/32 | base << 36)
+    const uint16_t *perm;   // SELL-sigma: storage position -> row within its 1024-row tile
+                            // (rows of a tile sorted by length; nullptr: identity)
 };
+
+// Natural row of storage position `pos` (SELL-sigma permutes rows inside
+// their tile only, so tiles and the canonical tile order are unchanged).
+__device__ __forceinline__ int64_t sell_row(const SellMatrix &A, int64_t pos) {
+    return A.perm ? ((pos & ~(int64_t)1023) + __ldg(A.perm + pos)) : pos;
+}
 
 // Format tag of the slice-shared-offset layout (the column-type template
 // parameter of the walks, next to int16_t / int32_t).

@@ -18,6 +18,7 @@ struct SellMatrixOwned {
     void *cols = nullptr;
     double *vals = nullptr;
     uint64_t *om = nullptr;  // slice-shared-offset pattern table (dia layout)
+    uint16_t *perm = nullptr;  // SELL-sigma row permutation (common.cuh: sell_row)
     int64_t n_patterns_words = 0;
     // dia layout, host copies: the pattern table and the slice descriptors
     // (start/32 | base << 36), used to plan the windowed SpMV (cg.cu: K1W)

@@ -17,8 +17,8 @@ __global__ void __launch_bounds__(TILE_THREADS) spmv_kernel(SellMatrix A, const 
     const int64_t base = (int64_t)blockIdx.x * TILE + threadIdx.x;
 #pragma unroll 1
     for (int j = 0; j < TILE_ELEMS; j++) {
-        int64_t row = base + j * TILE_THREADS;
-        if (row < A.n_rows) store<W>(y, ldy, row, spmv_row<M, 8, CT>(A, x, ldx, row));
+        int64_t pos = base + j * TILE_THREADS;  // storage position; output at its natural row
+        if (pos < A.n_rows) store<W>(y, ldy, sell_row(A, pos), spmv_row<M, 8, CT>(A, x, ldx, pos));
     }
 }
 

@@ -106,10 +106,12 @@ __device__ __forceinline__ mw::V<mw::Arith<M>::W> spmv_row_sell(const SellMatrix
                                                                 int64_t row, SliceWords sw) {
     using Ar = mw::Arith<M>;
     constexpr int W = Ar::W;
+    // `row` is the storage position (slice row); columns decode against the
+    // natural row (SELL-sigma: sell_row)
     const int64_t s0 = sw.w0;
     const int L = (int)((sw.w1 - s0) >> 5);
     const int64_t off = s0 + (row & 31);
-    const int grow = (int)(A.row_base + row);  // n_cols < 2^31 (sell.cu)
+    const int grow = (int)(A.row_base + (std::is_same<CT, int16_t>::value ? sell_row(A, row) : row));
     const CT *__restrict__ cp = (const CT *)A.cols + off;
     const double *__restrict__ vp = A.vals + off;
     mw::V<W> s = mw::zero<W>();

@@ -117,7 +117,8 @@ def device_matrix(A, row_base=0, col_format=-1):
     """SELL-32 device copy of a CsrMatrix, built once and cached on A.
     row_base: global index of row 0 when A holds a rank's rows with global
     columns (dist.py); col_format: -1 auto / 0 int32 / 1 int16 deltas /
-    2 slice-shared offsets (include/mwcg_cuda.h)."""
+    2 slice-shared offsets, optionally | _lib.SELL_SIGMA / _lib.SELL_NO_SIGMA
+    ("auto" is 15 with a flag) (include/mwcg_cuda.h)."""
     h = getattr(A, "_device", None)
     if h is not None:
         return h
@@ -156,6 +157,10 @@ class _DeviceMatrix:
 
     def col_bytes(self):
         return int(_lib.load().mwcg_matrix_col_bytes(self.handle))
+
+    def sigma_sorted(self):
+        """True when the SELL rows of each tile are stored length-sorted."""
+        return bool(_lib.load().mwcg_matrix_sigma_sorted(self.handle))
 
     def padded_entries(self):
         out = ctypes.c_int64()
