@@ -99,9 +99,18 @@ int mwcg_matrix_create(mwcg_matrix **out, int64_t n_rows, int64_t n_cols, int64_
  * each 1024-row tile by length (SELL-sigma, sigma = 1024) when that cuts the
  * slice padding by >= 5 %; OR-ing MWCG_SELL_SIGMA forces the sort,
  * MWCG_SELL_NO_SIGMA disables it (with a flag, "auto" is written 15).  Row
- * results are unchanged (each row is still summed left to right). */
+ * results are unchanged (each row is still summed left to right).
+ *
+ * Slice-shared layout, value-uniform slices: when every slot of a 32-row
+ * slice holds the same value bits in all the rows that have it (constant-
+ * coefficient stencils), the value is kept once per slot in the slice's
+ * pattern record and the slice streams no matrix bytes; slices that are not
+ * uniform stream their values as before.  MWCG_DIA_STREAM_VALUES turns the
+ * detection off (every slice streams its values).  Bitwise-identical
+ * results either way. */
 #define MWCG_SELL_SIGMA 16
 #define MWCG_SELL_NO_SIGMA 32
+#define MWCG_DIA_STREAM_VALUES 64
 int mwcg_matrix_create_ex(mwcg_matrix **out, int64_t n_rows, int64_t n_cols, int64_t nnz,
                           const void *row_ptr, const void *col_idx, const double *values,
                           int index_bytes, int64_t row_base, int col_format, void *stream);
@@ -110,6 +119,9 @@ int mwcg_matrix_sigma_sorted(const mwcg_matrix *A); /* 1 if the rows of each til
 int mwcg_matrix_destroy(mwcg_matrix *A);
 int mwcg_matrix_info(const mwcg_matrix *A, int64_t *n_rows, int64_t *n_cols, int64_t *nnz,
                      int64_t *padded_entries);
+/* value entries the layout stores (and streams per SpMV): padded_entries,
+ * minus the entries of value-uniform slices (slice-shared layout) */
+int64_t mwcg_matrix_stored_values(const mwcg_matrix *A);
 
 /* ---- operator table: replaces _fast.KERNELS[mode][op] (_fast.py:592-633) ---- */
 /* spmv_<mode> (_fast.py:284-290, 329-339, 383-393, 443-455, 501-513) */

@@ -18,7 +18,7 @@ STATUS = {0: "running", 1: "converged", 2: "max_iterations", 3: "breakdown"}
 STAGE = {"init": 0, "final_init": 1, "spmv": 2, "final_alpha": 3, "update": 4, "final_beta": 5,
          "xpay": 6, "spmv_interior": 7, "spmv_boundary": 8}
 ERR_VALUE = 1001
-SELL_SIGMA, SELL_NO_SIGMA = 16, 32  # col_format flags (include/mwcg_cuda.h)
+SELL_SIGMA, SELL_NO_SIGMA, DIA_STREAM_VALUES = 16, 32, 64  # col_format flags (include/mwcg_cuda.h)
 
 c_i64 = ctypes.c_int64
 c_dp = ctypes.POINTER(ctypes.c_double)
@@ -66,6 +66,7 @@ SIGNATURES = {
                                              c_vp, ctypes.c_int, c_i64, ctypes.c_int, c_vp]),
     "mwcg_matrix_col_bytes": (ctypes.c_int, [c_vp]),
     "mwcg_matrix_destroy": (ctypes.c_int, [c_vp]),
+    "mwcg_matrix_stored_values": (c_i64, [c_vp]),
     "mwcg_matrix_info": (ctypes.c_int, [c_vp, ctypes.POINTER(c_i64), ctypes.POINTER(c_i64),
                                         ctypes.POINTER(c_i64), ctypes.POINTER(c_i64)]),
     "mwcg_spmv": (ctypes.c_int, [ctypes.c_int, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp]),

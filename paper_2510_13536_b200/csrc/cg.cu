@@ -194,13 +194,22 @@ struct SpTraits {
 #ifdef MWCG_SP_MINB_OVERRIDE
     static constexpr int MINB = MWCG_SP_MINB_OVERRIDE;
 #else
-    static constexpr int MINB = (M == FP64) ? 3 : ((M == TW || M == QTW) ? 4 : 5);
+    // 4 CTAs of 256 threads (64 registers): the row walk holds a chunk of
+    // records and gathers plus the running sums without spilling (DW C2 K1
+    // 49.5 us at 5 CTAs / 48 registers, 43.4 us at 4 / 64)
+    static constexpr int MINB = (M == FP64) ? 3 : 4;
 #endif
     static constexpr int RPT = TILE / THREADS;
 #ifdef MWCG_SP_U_OVERRIDE
     static constexpr int U = MWCG_SP_U_OVERRIDE;
 #else
     static constexpr int U = (M == FP64) ? 8 : ((M == TW) ? 3 : 4);  // measured per mode (C2)
+#endif
+    // chunk of a value-uniform slice (no value registers: ops.cuh)
+#ifdef MWCG_SP_UU_OVERRIDE
+    static constexpr int UU = MWCG_SP_UU_OVERRIDE;
+#else
+    static constexpr int UU = U;
 #endif
 };
 
@@ -211,7 +220,6 @@ __global__ void __launch_bounds__(SpTraits<M>::THREADS, SpTraits<M>::MINB)
     using Ar = Arith<M>;
     constexpr int W = Ar::W;
     constexpr int NT = SpTraits<M>::THREADS;
-    constexpr int RPT = SpTraits<M>::RPT;
     // 256 threads: thread t owns rows t + 256 j, which IS the canonical tile
     // mapping, so its p.q terms accumulate in registers in canonical order;
     // 512 threads (FP64) and the SELL layouts (whose rows may be sorted by
@@ -223,40 +231,51 @@ __global__ void __launch_bounds__(SpTraits<M>::THREADS, SpTraits<M>::MINB)
     __shared__ int s_last;
     if (stopped_k1(st, h, use_cond)) return;
     const bool norm_all = st->norm_all != 0;
-    const int64_t n = g.n;
+    // rows < 2^31 (sell_create): tile and row indices are 32-bit, so the
+    // per-row address arithmetic is one wide multiply-add per access
+    const int n = (int)g.n;
     const int dir = (int)(st->k & 1);
-    const int64_t cnt = k1_count(g);
-    for (int64_t t = blockIdx.x; t < cnt; t += gridDim.x) {
-        const int64_t tile = k1_tile(g, snake(t, cnt, dir));
-        // the next row's slice words are loaded while this row walks (they
-        // head its dependency chain)
-        SliceWords nsw = slice_words(A, tile * TILE + threadIdx.x);
+    const int cnt = (int)k1_count(g), cnt_a = (int)(g.a1 - g.a0);
+    const double *__restrict__ pl = p + g.p_off * W;  // the local slice of p (AoS)
+    for (int t = blockIdx.x; t < cnt; t += gridDim.x) {
+        const int ts = dir ? cnt - 1 - t : t;  // snake order
+        const int tile = ts < cnt_a ? (int)g.a0 + ts : (int)g.b0 + (ts - cnt_a);
+        // storage position of the thread's current row; the tile and the row
+        // count are read back from it (tile = pos >> 10, last row when
+        // pos + NT leaves the tile), so the row loop carries one index
+        int pos = tile * TILE + (int)threadIdx.x;
+        SliceWords sw = slice_words<CT>(A, pos);
         V<W> acc = zero<W>();
 #pragma unroll 1
-        for (int k = 0; k < RPT; k++) {
-            const int lp = threadIdx.x + k * NT;  // storage position inside the tile
-            const int64_t pos = tile * TILE + lp;
-            const SliceWords sw = nsw;
-            if (k + 1 < RPT) nsw = slice_words(A, pos + NT);
+        for (;;) {
+            const bool more = ((pos + NT) >> 10) == (pos >> 10);
             V<W> term = zero<W>();
-            const int64_t row = std::is_same<CT, DiaTag>::value ? pos : sell_row(A, pos);
+            const int row = std::is_same<CT, DiaTag>::value ? pos : (int)sell_row(A, pos);
             if (pos < n) {
                 // columns are global: p is the full (replicated) vector
-                V<W> sv = spmv_row<M, SpTraits<M>::U, CT, true>(A, p, 0, pos, sw);
+                V<W> sv = spmv_row<M, SpTraits<M>::U, CT, true, SpTraits<M>::UU>(A, p, 0, pos, sw);
+                // the next row's slice words head its dependency chain: their
+                // load is issued here, under this row's p.q term
+                if (more) sw = slice_words<CT>(A, pos + NT);
                 if (norm_all) sv = Ar::norm(sv);
-                store<W>(q, g.ld, row, sv);
-                if (FUSED) term = Ar::mul(load_aos_ro<W>(p, g.p_off + row), sv);
+                store<W>(q + row, g.ld, 0, sv);
+                if (FUSED) term = Ar::mul(load_aos_ro<W>(pl + (int64_t)row * W, 0), sv);
                 if (FUSED && !STAGE) acc = Ar::add(acc, term);
+            } else if (more) {
+                sw = slice_words<CT>(A, pos + NT);
             }
             if (STAGE) {
 #pragma unroll
-                for (int w = 0; w < W; w++) terms[w * TILE + (row - tile * TILE)] = term.w[w];
+                for (int w = 0; w < W; w++) terms[w * TILE + (row & (TILE - 1))] = term.w[w];
             }
+            if (!more) break;
+            pos += NT;
         }
+        const int tile2 = pos >> 10;
         if (STAGE) {
             __syncthreads();
             if (threadIdx.x < TILE_THREADS) {
-                const int64_t base = tile * TILE + threadIdx.x;
+                const int base = tile2 * TILE + (int)threadIdx.x;
 #pragma unroll
                 for (int j = 0; j < TILE_ELEMS; j++) {
                     if (base + j * TILE_THREADS < n) {
@@ -270,7 +289,7 @@ __global__ void __launch_bounds__(SpTraits<M>::THREADS, SpTraits<M>::MINB)
         }
         if (FUSED) {
             acc = block_tree_first<M, TILE_THREADS>(acc, smem);
-            if (threadIdx.x == 0) store_part<W>(part, g.part_ld, g.tile_off + tile, acc);
+            if (threadIdx.x == 0) store_part<W>(part, g.part_ld, g.tile_off + tile2, acc);
         }
     }
     if (!FUSED || !g.final_) return;
@@ -1243,6 +1262,8 @@ int mwcg_matrix_sigma_sorted(const mwcg_matrix *A) { return A && A->M->view.perm
 int mwcg_matrix_col_bytes(const mwcg_matrix *A) {
     return A ? (A->M->view.dia ? 0 : (A->M->view.col16 ? 2 : 4)) : -1;
 }
+
+int64_t mwcg_matrix_stored_values(const mwcg_matrix *A) { return A ? A->M->view.stored : -1; }
 
 int mwcg_matrix_destroy(mwcg_matrix *A) {
     if (A) {

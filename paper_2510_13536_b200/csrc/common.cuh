@@ -41,6 +41,13 @@ inline int64_t num_tiles(int64_t n) { return (n + TILE - 1) / TILE; }
 // left-to-right sum is unchanged; no column array is streamed, and a row's
 // gathers depend only on the (L1-resident, warp-uniform) offset word, not on
 // a column load from HBM.
+//
+// Slice-uniform values: when, in every slot of a slice, all present lanes hold
+// the SAME value bits (constant-coefficient stencils: every row of the slice
+// carries the same coefficient at a given offset), the slot's value is stored
+// once, next to its offset word, in the pattern record -- such a slice streams
+// no matrix bytes at all (its whole description is an L1-resident pattern).
+// The arithmetic and its order are unchanged: dxmul(a, x) sees the same a.
 constexpr int16_t COL16_SENT = -32768;
 constexpr int32_t COL32_SENT = -1;
 
@@ -49,15 +56,17 @@ struct SellMatrix {
     int64_t n_cols;
     int64_t nnz;
     int64_t n_slices;
-    int64_t total;          // padded entry count
+    int64_t total;          // padded entry count (slots * 32, all slices)
+    int64_t stored;         // value entries actually stored (dia: non-uniform slices only)
     int64_t row_base;       // global index of local row 0 (row-partitioned ranks)
     int col16;              // 1: int16 deltas, 0: int32 absolute
     int dia;                // 1: slice-shared offsets (om; no column array)
     const int64_t *slice_ptr;
     const void *cols;
     const double *vals;
-    const uint64_t *om;     // dia: pattern table of slot words (lane mask << 32 | uint32 offset);
-                            // slice_ptr then holds descriptors (start/32 | base << 36)
+    const ulonglong2 *pat;  // dia: pattern table of slot records {lane mask << 32 | uint32 offset,
+                            // uniform value bits}; slice_ptr then holds two descriptor words
+                            // per slice: {start/32 | L << 40 | uniform << 48, pattern base}
     const uint16_t *perm;   // SELL-sigma: storage position -> row within its 1024-row tile
                             // (rows of a tile sorted by length; nullptr: identity)
 };

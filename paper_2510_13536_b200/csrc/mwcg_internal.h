@@ -17,17 +17,13 @@ struct SellMatrixOwned {
     int64_t *slice_ptr = nullptr;
     void *cols = nullptr;
     double *vals = nullptr;
-    uint64_t *om = nullptr;  // slice-shared-offset pattern table (dia layout)
+    ulonglong2 *pat = nullptr;  // slice-shared-offset pattern table (dia layout)
     uint16_t *perm = nullptr;  // SELL-sigma row permutation (common.cuh: sell_row)
     int64_t n_patterns_words = 0;
-    // dia layout, host copies: the pattern table and the slice descriptors
-    // (start/32 | base << 36), used to plan the windowed SpMV (cg.cu: K1W)
-    std::vector<uint64_t> pat_host, desc_host;
 };
 
-// slice descriptors are padded with this many copies of the last one, so a
-// bulk copy of a stage's descriptors may run past the last slice
-constexpr int DESC_PAD = 64;
+// the dia descriptor table is padded with this many empty slices
+constexpr int DESC_PAD = 2;
 
 // col_format: -1 auto (slice-shared offsets when they pay, else int16 deltas
 // when they fit, else int32), 0 force int32, 1 force int16, 2 force slice-shared

@@ -37,65 +37,164 @@ struct ColCodec<int32_t> {  // absolute int32 column
     static __device__ __forceinline__ int col(int, int32_t d) { return d; }
 };
 
-// The two slice words a row's walk starts from (slice_ptr[s], slice_ptr[s+1]:
-// entry offsets, or dia descriptors).  Loading them is the first link of
-// the row's dependency chain, so callers that walk several rows load the
-// next row's words ahead (cg_spmv_pq).  Rows past the last slice clamp to
-// it (their results are discarded).
+// The two slice words a row's walk starts from: slice_ptr[s], slice_ptr[s+1]
+// (entry offsets, SELL layouts) or the slice's descriptor pair (dia layout,
+// one 16-B load).  Loading them is the first link of the row's dependency
+// chain, so callers that walk several rows load the next row's words ahead
+// (cg_spmv_pq).  Rows past the last slice clamp to it (their results are
+// discarded).
 struct SliceWords {
     int64_t w0, w1;
 };
+template <typename CT>
 __device__ __forceinline__ SliceWords slice_words(const SellMatrix &A, int64_t row) {
-    const int64_t sl = min(row >> 5, A.n_slices - 1);
-    return SliceWords{__ldg(A.slice_ptr + sl), __ldg(A.slice_ptr + sl + 1)};
+    const int sl = min((int)(row >> 5), (int)A.n_slices - 1);  // rows < 2^31
+    if constexpr (std::is_same<CT, DiaTag>::value) {
+        const longlong2 d = __ldg(reinterpret_cast<const longlong2 *>(A.slice_ptr) + sl);
+        return SliceWords{d.x, d.y};
+    } else {
+        return SliceWords{__ldg(A.slice_ptr + sl), __ldg(A.slice_ptr + sl + 1)};
+    }
 }
 
-// Slice-shared-offset walk: the U slot words (warp-uniform broadcast loads
+// Slice-shared-offset walk: the U slot records (warp-uniform broadcast loads
 // from the L1-resident pattern table) and the U values issue together; each
 // gather's address depends only on its slot word, so the gathers overlap the
-// value stream.  Every pattern in the table is followed by DIA_PAD zero words
-// and the value array by DIA_PAD slots, so a chunk reads past the slice's
-// last slot without clamping: those slots have an empty lane mask.  A lane
-// without an entry in a slot gathers its own row (always in bounds) and
-// skips the arithmetic.
+// value stream.  Every pattern in the table is followed by DIA_PAD zero
+// records and the value array by DIA_PAD slots, so a chunk reads past the
+// slice's last slot without clamping: those slots have an empty lane mask.  A
+// lane without an entry in a slot gathers its own row (always in bounds) and
+// skips the arithmetic.  A slice whose slots are value-uniform (descriptor
+// flag) takes its values from the records and streams nothing.
 constexpr int DIA_PAD = 8;  // >= the largest U
+constexpr int DIA_LBITS = 40;                       // descriptor word 0: start/32 | L << 40 | uniform << 48
+constexpr uint64_t DIA_START_MASK = (1ull << DIA_LBITS) - 1;
+constexpr int DIA_MAX_SLOTS = 255;
 
-template <int M, int U, bool XAOS>
+// base + off * SCALE bytes as ONE wide multiply-add (IMAD.WIDE); written in
+// PTX because the compiler otherwise sign-extends the offset and adds the
+// halves separately (three instructions per gather).
+template <int SCALE>
+__device__ __forceinline__ const double *wide_offset(const double *base, int off) {
+    const double *r;
+    asm("mad.wide.s32 %0, %1, %2, %3;" : "=l"(r) : "r"(off), "n"(SCALE), "l"(base));
+    return r;
+}
+
+// Gather of x at (row + off): the row's own record address xg (computed once
+// per row) plus a 32-bit offset.
+template <int W, bool XAOS>
+__device__ __forceinline__ mw::V<W> dia_gather(const double *__restrict__ xg, int64_t ldx, int off) {
+    mw::V<W> r;
+    if (XAOS) {
+        const double *__restrict__ e = wide_offset<8 * W>(xg, off);
+        if (W == 2) {
+            const double2 t = __ldg(reinterpret_cast<const double2 *>(e));
+            r.w[0] = t.x;
+            r.w[W - 1] = t.y;
+        } else {
+#pragma unroll
+            for (int k = 0; k < W; k++) r.w[k] = __ldg(e + k);
+        }
+    } else {
+        const double *__restrict__ e = wide_offset<8>(xg, off);
+#pragma unroll
+        for (int k = 0; k < W; k++) r.w[k] = __ldg(e + k * ldx);
+    }
+    return r;
+}
+
+// s = ok ? t : s, word by word (a lane without an entry in the slot keeps its sum)
+template <int W>
+__device__ __forceinline__ mw::V<W> keep_if(bool ok, mw::V<W> t, mw::V<W> s) {
+#pragma unroll
+    for (int k = 0; k < W; k++) s.w[k] = ok ? t.w[k] : s.w[k];
+    return s;
+}
+
+// One chunk of N slots of a slice-shared-offset row.  The N records (and,
+// for a streamed slice, the N values) are loaded first, then the N gathers
+// issue, then the arithmetic runs -- branch-free: a lane without an entry in
+// a slot gathers its own row (always in bounds), multiplies, and keeps its
+// old sum by a select.  (With a branch on the lane predicate the compiler
+// sinks each slot's loads into its branch: one memory round trip per entry.)
+template <int M, int N, bool XAOS, bool UNIFORM>
+__device__ __forceinline__ void dia_chunk(mw::V<mw::Arith<M>::W> &s, const ulonglong2 *__restrict__ op,
+                                          const double *__restrict__ vp, const double *__restrict__ xg,
+                                          int64_t ldx, uint32_t lbit) {
+    using Ar = mw::Arith<M>;
+    constexpr int W = Ar::W;
+    double a[N];
+    bool ok[N];
+    mw::V<W> xv[N];
+#pragma unroll
+    for (int u = 0; u < N; u++) {
+        uint64_t om;
+        if (UNIFORM) {
+            const ulonglong2 rec = __ldg(op + u);
+            om = rec.x;
+            a[u] = __longlong_as_double((long long)rec.y);
+        } else {
+            om = __ldg(&op[u].x);
+            a[u] = ld_stream(vp + u * SLICE);
+        }
+        ok[u] = ((uint32_t)(om >> 32) & lbit) != 0;
+        xv[u] = dia_gather<W, XAOS>(xg, ldx, ok[u] ? (int)(uint32_t)om : 0);
+    }
+    // streamed TW/QTW rows keep the lane branch (C4 QTW K1: 78 us against
+    // 87 us branch-free; every other case is as fast or faster branch-free)
+    constexpr bool BRANCHY = !UNIFORM && W == 3;
+#pragma unroll
+    for (int u = 0; u < N; u++) {
+        if (BRANCHY) {
+            if (ok[u]) s = Ar::add(s, Ar::dxmul(a[u], xv[u]));
+        } else {
+            s = keep_if<W>(ok[u], Ar::add(s, Ar::dxmul(a[u], xv[u])), s);
+        }
+    }
+}
+
+// the slots of a row: full chunks of U, then one exact chunk for the rest
+template <int M, int U, bool XAOS, bool UNIFORM>
+__device__ __forceinline__ void dia_walk(mw::V<mw::Arith<M>::W> &s, int L, const ulonglong2 *__restrict__ op,
+                                         const double *__restrict__ vp, const double *__restrict__ xg,
+                                         int64_t ldx, uint32_t lbit) {
+    int k0 = 0;
+    for (; k0 + U <= L; k0 += U, op += U, vp += U * SLICE) dia_chunk<M, U, XAOS, UNIFORM>(s, op, vp, xg, ldx, lbit);
+    const int rem = L - k0;
+    if (U > 1 && rem == 1) dia_chunk<M, 1, XAOS, UNIFORM>(s, op, vp, xg, ldx, lbit);
+    if (U > 2 && rem == 2) dia_chunk<M, 2, XAOS, UNIFORM>(s, op, vp, xg, ldx, lbit);
+    if (U > 3 && rem == 3) dia_chunk<M, 3, XAOS, UNIFORM>(s, op, vp, xg, ldx, lbit);
+    if (U > 4 && rem >= 4) {  // U up to 8: 4 + (rem - 4)
+        dia_chunk<M, 4, XAOS, UNIFORM>(s, op, vp, xg, ldx, lbit);
+        op += 4;
+        vp += 4 * SLICE;
+        if (rem == 5) dia_chunk<M, 1, XAOS, UNIFORM>(s, op, vp, xg, ldx, lbit);
+        if (rem == 6) dia_chunk<M, 2, XAOS, UNIFORM>(s, op, vp, xg, ldx, lbit);
+        if (rem == 7) dia_chunk<M, 3, XAOS, UNIFORM>(s, op, vp, xg, ldx, lbit);
+    }
+}
+
+template <int M, int U, bool XAOS, int UU = U>
 __device__ __forceinline__ mw::V<mw::Arith<M>::W> spmv_row_dia(const SellMatrix &A,
                                                                const double *__restrict__ x, int64_t ldx,
                                                                int64_t row, SliceWords sw) {
-    static_assert(U <= DIA_PAD, "pattern padding must cover a chunk");
+    static_assert(U <= 8 && UU <= 8, "chunk tails cover U <= 8");
     using Ar = mw::Arith<M>;
     constexpr int W = Ar::W;
-    // slice descriptor: (start / 32) | (pattern base << 36)  (sell.cu: dia_patterns)
-    constexpr uint64_t LO = (1ull << 36) - 1;
-    const uint64_t d0 = (uint64_t)sw.w0, d1 = (uint64_t)sw.w1;
-    const int64_t s0 = (int64_t)(d0 & LO) << 5;
-    const int L = (int)((d1 & LO) - (d0 & LO));
-    const int lane = (int)(row & 31);
-    const int grow = (int)(A.row_base + row);
-    const uint64_t *__restrict__ op = A.om + (d0 >> 36);
-    const double *__restrict__ vp = A.vals + s0 + lane;
+    const uint64_t d0 = (uint64_t)sw.w0;
+    const int L = (int)((uint32_t)(d0 >> DIA_LBITS) & 0xffu);
+    const bool uniform = ((uint32_t)(d0 >> DIA_LBITS) & 0x100u) != 0;
+    const uint32_t lbit = 1u << ((int)row & 31);
+    // the row's own element: every gather is this address + a slot offset
+    const double *__restrict__ xg = x + (A.row_base + row) * (XAOS ? W : 1);
+    const ulonglong2 *__restrict__ op = A.pat + sw.w1;
     mw::V<W> s = mw::zero<W>();
-    for (int k0 = 0; k0 < L; k0 += U, op += U, vp += U * SLICE) {
-        uint64_t om[U];
-        double a[U];
-#pragma unroll
-        for (int u = 0; u < U; u++) {
-            om[u] = __ldg(op + u);
-            a[u] = ld_stream(vp + u * SLICE);
-        }
-        bool ok[U];
-        mw::V<W> xv[U];
-#pragma unroll
-        for (int u = 0; u < U; u++) {
-            ok[u] = (uint32_t)(om[u] >> 32) & (1u << lane);
-            const int c = grow + (ok[u] ? (int)(uint32_t)om[u] : 0);
-            xv[u] = XAOS ? mw::load_aos_ro<W>(x, c) : mw::load_ro<W>(x, ldx, c);
-        }
-#pragma unroll
-        for (int u = 0; u < U; u++)
-            if (ok[u]) s = Ar::add(s, Ar::dxmul(a[u], xv[u]));
+    if (uniform) {
+        dia_walk<M, UU, XAOS, true>(s, L, op, nullptr, xg, ldx, lbit);
+    } else {
+        const double *__restrict__ vp = A.vals + (((int64_t)(d0 & DIA_START_MASK) << 5) + ((int)row & 31));
+        dia_walk<M, U, XAOS, false>(s, L, op, vp, xg, ldx, lbit);
     }
     return s;
 }
@@ -139,18 +238,18 @@ __device__ __forceinline__ mw::V<mw::Arith<M>::W> spmv_row_sell(const SellMatrix
 }
 
 // one row of y = A x in the matrix's layout
-template <int M, int U, typename CT, bool XAOS = false>
+template <int M, int U, typename CT, bool XAOS = false, int UU = U>
 __device__ __forceinline__ mw::V<mw::Arith<M>::W> spmv_row(const SellMatrix &A,
                                                            const double *__restrict__ x, int64_t ldx,
                                                            int64_t row, SliceWords sw) {
-    if constexpr (std::is_same<CT, DiaTag>::value) return spmv_row_dia<M, U, XAOS>(A, x, ldx, row, sw);
+    if constexpr (std::is_same<CT, DiaTag>::value) return spmv_row_dia<M, U, XAOS, UU>(A, x, ldx, row, sw);
     else return spmv_row_sell<M, U, CT, XAOS>(A, x, ldx, row, sw);
 }
 template <int M, int U, typename CT, bool XAOS = false>
 __device__ __forceinline__ mw::V<mw::Arith<M>::W> spmv_row(const SellMatrix &A,
                                                            const double *__restrict__ x, int64_t ldx,
                                                            int64_t row) {
-    return spmv_row<M, U, CT, XAOS>(A, x, ldx, row, slice_words(A, row));
+    return spmv_row<M, U, CT, XAOS>(A, x, ldx, row, slice_words<CT>(A, row));
 }
 
 // dispatch helper: F(CT) with the matrix's format tag / column type

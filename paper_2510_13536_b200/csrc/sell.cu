@@ -10,6 +10,7 @@
 // unchanged.
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <unordered_map>
 #include <vector>
 #include <cub/cub.cuh>
@@ -116,15 +117,21 @@ __global__ void sigma_slice_kernel(const I *__restrict__ rp, int64_t n_rows, con
 // CSR entries in lock-step by ascending column offset (warp min over the
 // lanes' heads); every distinct offset becomes one slot with the ballot of
 // the lanes that have it.  Pass 1 counts slots (capped: a slice needing more
-// than cap = Lmax + DIA_SLACK slots marks the matrix as not DIA-friendly);
-// pass 2 writes the slot words and the values.
+// than cap = Lmax + DIA_SLACK slots, or more than DIA_MAX_SLOTS, marks the
+// matrix as not DIA-friendly) and decides whether the slice is value-uniform
+// (every slot: all present lanes hold the same value bits); pass 2 writes the
+// slot records (offset word + uniform value) and, for the other slices, the
+// per-lane values.
 // ---------------------------------------------------------------------------
 constexpr int DIA_SLACK = 2;
+constexpr int DIA_UNIFORM_BIT = 1 << 8;  // slice_info: slots | uniform << 8
 
 template <typename I, bool FILL>
 __global__ void dia_walk_kernel(const I *__restrict__ rp, const I *__restrict__ ci, const double *__restrict__ va,
-                                int64_t n_rows, int64_t n_slices, int64_t row_base, int64_t *__restrict__ slice_sz,
-                                const int64_t *__restrict__ slice_ptr, uint64_t *__restrict__ om,
+                                int64_t n_rows, int64_t n_slices, int64_t row_base, int allow_uniform,
+                                int64_t *__restrict__ val_sz, int64_t *__restrict__ rec_sz,
+                                int32_t *__restrict__ slice_info, const int64_t *__restrict__ val_ptr,
+                                const int64_t *__restrict__ rec_ptr, ulonglong2 *__restrict__ rec,
                                 double *__restrict__ vals, unsigned int *__restrict__ reject) {
     const int64_t sl = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
@@ -138,9 +145,11 @@ __global__ void dia_walk_kernel(const I *__restrict__ rp, const I *__restrict__ 
     int len = (int)(hi - head);
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) len = max(len, __shfl_xor_sync(0xffffffffu, len, off));
-    const int cap = len + DIA_SLACK;
+    const int cap = min(len + DIA_SLACK, DIA_MAX_SLOTS);
     const int64_t g = row_base + r;
-    const int64_t s0 = FILL ? slice_ptr[sl] : 0;
+    bool uniform = FILL ? (slice_info[sl] & DIA_UNIFORM_BIT) != 0 : allow_uniform != 0;
+    const int64_t v0 = FILL ? val_ptr[sl] : 0;
+    const int64_t r0 = FILL ? rec_ptr[sl] : 0;
     int k = 0;
     for (;;) {
         const int cur = head < hi ? (int)((int64_t)ci[head] - g) : INT_MAX;
@@ -152,69 +161,85 @@ __global__ void dia_walk_kernel(const I *__restrict__ rp, const I *__restrict__ 
             if (lane == 0) atomicOr(reject, 1u);
             break;
         }
+        const unsigned long long bits = present ? (unsigned long long)__double_as_longlong(va[head]) : 0ull;
+        // value bits of the first present lane
+        const unsigned long long first = __shfl_sync(0xffffffffu, bits, __ffs((int)mask) - 1);
+        if (!FILL) uniform = uniform && __all_sync(0xffffffffu, !present || bits == first);
         if (FILL) {
-            if (lane == 0) om[(s0 >> 5) + k] = ((uint64_t)mask << 32) | (uint64_t)(uint32_t)m;
-            vals[s0 + (int64_t)k * SLICE + lane] = present ? va[head] : 0.0;
+            if (lane == 0)
+                rec[r0 + k] = make_ulonglong2(((unsigned long long)mask << 32) | (unsigned long long)(uint32_t)m,
+                                              uniform ? first : 0ull);
+            if (!uniform) vals[v0 + (int64_t)k * SLICE + lane] = __longlong_as_double((long long)bits);
         }
         if (present) head++;
         k++;
     }
-    if (!FILL && lane == 0) slice_sz[sl] = (int64_t)k * SLICE;
+    if (!FILL && lane == 0) {
+        val_sz[sl] = uniform ? 0 : (int64_t)k * SLICE;
+        rec_sz[sl] = k;
+        slice_info[sl] = k | (uniform ? DIA_UNIFORM_BIT : 0);
+    }
 }
 
-// Slot-word patterns: stencil and band slices repeat a handful of (offset,
-// mask) sequences (interior / boundary combinations), so the slot words are
-// deduplicated into a pattern table small enough to stay in L1, and each
-// slice's descriptor packs its value offset with its pattern base:
-//   desc[j] = (slice_start / 32) | (pattern_base << 36),
-// desc[n_slices] = total / 32.  A row's gathers then wait on one L2 load
-// (desc) and one L1 hit (the pattern word) instead of two L2 loads.
-static int dia_patterns(SellMatrixOwned *M, int64_t *slice_ptr, int64_t n_words, cudaStream_t st) {
+// Slot-record patterns: stencil and band slices repeat a handful of (offset,
+// mask[, value]) sequences (interior / boundary combinations), so the slot
+// records are deduplicated into a pattern table small enough to stay in L1,
+// and each slice gets a two-word descriptor
+//   { value_start / 32 | slots << 40 | uniform << 48,  pattern base }.
+// A row's gathers then wait on one L2 load (the descriptor) and one L1 hit
+// (the pattern record) instead of two L2 loads.
+static int dia_patterns(SellMatrixOwned *M, const int64_t *val_ptr, const int64_t *rec_ptr,
+                        const int32_t *slice_info, const ulonglong2 *rec, int64_t n_rec, cudaStream_t st) {
     SellMatrix &A = M->view;
     const int64_t ns = A.n_slices;
-    std::vector<int64_t> sp(ns + 1);
-    std::vector<uint64_t> om(n_words);
-    MWCG_CUDA(cudaMemcpyAsync(sp.data(), slice_ptr, sizeof(int64_t) * (ns + 1), cudaMemcpyDeviceToHost, st));
-    MWCG_CUDA(cudaMemcpyAsync(om.data(), M->om, sizeof(uint64_t) * n_words, cudaMemcpyDeviceToHost, st));
+    std::vector<int64_t> vp(ns + 1), rp(ns + 1);
+    std::vector<int32_t> info(ns);
+    std::vector<ulonglong2> rc((size_t)n_rec);
+    MWCG_CUDA(cudaMemcpyAsync(vp.data(), val_ptr, sizeof(int64_t) * (ns + 1), cudaMemcpyDeviceToHost, st));
+    MWCG_CUDA(cudaMemcpyAsync(rp.data(), rec_ptr, sizeof(int64_t) * (ns + 1), cudaMemcpyDeviceToHost, st));
+    MWCG_CUDA(cudaMemcpyAsync(info.data(), slice_info, sizeof(int32_t) * ns, cudaMemcpyDeviceToHost, st));
+    if (n_rec > 0)
+        MWCG_CUDA(cudaMemcpyAsync(rc.data(), rec, sizeof(ulonglong2) * (size_t)n_rec, cudaMemcpyDeviceToHost, st));
     MWCG_CUDA(cudaStreamSynchronize(st));
-    std::vector<uint64_t> pat;
-    std::vector<uint64_t> desc(ns + 1);
+    std::vector<ulonglong2> pat;
+    std::vector<uint64_t> desc(2 * (size_t)(ns + DESC_PAD));
     std::unordered_multimap<uint64_t, std::pair<int64_t, int64_t>> seen;  // hash -> (pattern base, length)
+    auto same = [](const ulonglong2 &a, const ulonglong2 &b) { return a.x == b.x && a.y == b.y; };
     for (int64_t j = 0; j < ns; j++) {
-        const int64_t b = sp[j] >> 5, len = (sp[j + 1] - sp[j]) >> 5;
+        const int64_t b = rp[j], len = rp[j + 1] - rp[j];
         uint64_t hsh = 1469598103934665603ull ^ (uint64_t)len;
-        for (int64_t k = 0; k < len; k++) hsh = (hsh ^ om[b + k]) * 1099511628211ull;
+        for (int64_t k = 0; k < len; k++) {
+            hsh = (hsh ^ rc[b + k].x) * 1099511628211ull;
+            hsh = (hsh ^ rc[b + k].y) * 1099511628211ull;
+        }
         int64_t base = -1;
         auto rng = seen.equal_range(hsh);
         for (auto it = rng.first; it != rng.second && base < 0; ++it)
             if (it->second.second == len &&
-                std::equal(om.begin() + b, om.begin() + b + len, pat.begin() + it->second.first))
+                std::equal(rc.begin() + b, rc.begin() + b + len, pat.begin() + it->second.first, same))
                 base = it->second.first;
         if (base < 0) {
             base = (int64_t)pat.size();
-            pat.insert(pat.end(), om.begin() + b, om.begin() + b + len);
-            pat.insert(pat.end(), DIA_PAD, 0ull);  // empty slots: chunks may read past the end
+            pat.insert(pat.end(), rc.begin() + b, rc.begin() + b + len);
+            pat.insert(pat.end(), DIA_PAD, make_ulonglong2(0ull, 0ull));  // empty slots: chunks may read past the end
             seen.emplace(hsh, std::make_pair(base, len));
         }
-        if (base >= (1ll << 28)) {
-            set_error("slice-shared offsets: pattern table too large");
-            return MWCG_ERR_VALUE;
-        }
-        desc[j] = (uint64_t)(sp[j] >> 5) | ((uint64_t)base << 36);
+        const uint64_t uni = (info[j] & DIA_UNIFORM_BIT) ? 1ull : 0ull;
+        desc[2 * j] = (uint64_t)(vp[j] >> 5) | ((uint64_t)len << DIA_LBITS) | (uni << (DIA_LBITS + 8));
+        desc[2 * j + 1] = (uint64_t)base;
     }
-    desc[ns] = (uint64_t)(sp[ns] >> 5);
-    if (pat.empty()) pat.assign(DIA_PAD, 0ull);
-    pool_free(M->om, st);
-    M->om = nullptr;
-    MWCG_CUDA(pool_alloc((void **)&M->om, sizeof(uint64_t) * pat.size(), st));
-    MWCG_CUDA(cudaMemcpyAsync(M->om, pat.data(), sizeof(uint64_t) * pat.size(), cudaMemcpyHostToDevice, st));
-    desc.resize(ns + 1 + DESC_PAD, desc[ns]);
-    MWCG_CUDA(cudaMemcpyAsync(slice_ptr, desc.data(), sizeof(uint64_t) * desc.size(), cudaMemcpyHostToDevice, st));
+    if (pat.empty()) pat.assign(DIA_PAD, make_ulonglong2(0ull, 0ull));
+    // descriptors past the last slice: empty slices (L = 0) on the empty pattern
+    for (int64_t j = ns; j < ns + DESC_PAD; j++) {
+        desc[2 * j] = (uint64_t)(vp[ns] >> 5);
+        desc[2 * j + 1] = (uint64_t)(pat.size() - DIA_PAD);
+    }
+    MWCG_CUDA(pool_alloc((void **)&M->pat, sizeof(ulonglong2) * pat.size(), st));
+    MWCG_CUDA(cudaMemcpyAsync(M->pat, pat.data(), sizeof(ulonglong2) * pat.size(), cudaMemcpyHostToDevice, st));
+    MWCG_CUDA(pool_alloc((void **)&M->slice_ptr, sizeof(uint64_t) * desc.size(), st));
+    MWCG_CUDA(cudaMemcpyAsync(M->slice_ptr, desc.data(), sizeof(uint64_t) * desc.size(), cudaMemcpyHostToDevice, st));
     MWCG_CUDA(cudaStreamSynchronize(st));
     M->n_patterns_words = (int64_t)pat.size();
-    M->pat_host = std::move(pat);
-    desc.resize(ns + 1);
-    M->desc_host = std::move(desc);
     return 0;
 }
 
@@ -223,67 +248,85 @@ static int dia_patterns(SellMatrixOwned *M, int64_t *slice_ptr, int64_t n_words,
 // padded SELL layout, or offsets beyond int32), or an error code < 0 / > 1.
 template <typename I>
 static int build_dia(SellMatrixOwned *M, const I *rp, const I *ci, const double *va, int64_t sell_total,
-                     bool force, cudaStream_t st) {
+                     bool force, bool allow_uniform, cudaStream_t st) {
     SellMatrix &A = M->view;
     if (A.n_slices == 0) return 0;  // no rows: the (empty) SELL layout
-    int64_t *slice_sz = nullptr, *slice_ptr = nullptr;
+    const int64_t ns = A.n_slices;
+    int64_t *sz = nullptr, *ptr = nullptr;  // [0, ns]: value entries, [ns+1, 2ns+1]: records
+    int32_t *info = nullptr;
     unsigned int *flag = nullptr;
-    MWCG_CUDA(pool_alloc((void **)&slice_sz, sizeof(int64_t) * (A.n_slices + 1), st));
+    MWCG_CUDA(pool_alloc((void **)&sz, sizeof(int64_t) * 2 * (ns + 1), st));
+    MWCG_CUDA(pool_alloc((void **)&ptr, sizeof(int64_t) * 2 * (ns + 1), st));
+    MWCG_CUDA(pool_alloc((void **)&info, sizeof(int32_t) * ns, st));
     MWCG_CUDA(pool_alloc((void **)&flag, sizeof(unsigned int), st));
-    MWCG_CUDA(cudaMemsetAsync(slice_sz, 0, sizeof(int64_t) * (A.n_slices + 1), st));
+    MWCG_CUDA(cudaMemsetAsync(sz, 0, sizeof(int64_t) * 2 * (ns + 1), st));
     MWCG_CUDA(cudaMemsetAsync(flag, 0, sizeof(unsigned int), st));
-    const unsigned blocks = (unsigned)((A.n_slices * 32 + 255) / 256);
-    dia_walk_kernel<I, false><<<blocks, 256, 0, st>>>(rp, ci, va, A.n_rows, A.n_slices, A.row_base, slice_sz,
-                                                      nullptr, nullptr, nullptr, flag);
+    const unsigned blocks = (unsigned)((ns * 32 + 255) / 256);
+    dia_walk_kernel<I, false><<<blocks, 256, 0, st>>>(rp, ci, va, A.n_rows, ns, A.row_base, allow_uniform ? 1 : 0, sz,
+                                                      sz + ns + 1, info, nullptr, nullptr, nullptr, nullptr, flag);
     MWCG_CHECK_LAUNCH();
-    MWCG_CUDA(pool_alloc((void **)&slice_ptr, sizeof(int64_t) * (A.n_slices + 1 + DESC_PAD), st));
     size_t tmp_bytes = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, slice_sz, slice_ptr, A.n_slices + 1, st);
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, sz, ptr, ns + 1, st);
     void *tmp = nullptr;
     MWCG_CUDA(pool_alloc(&tmp, tmp_bytes, st));
-    MWCG_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, slice_sz, slice_ptr, A.n_slices + 1, st));
-    int64_t total = 0;
+    MWCG_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, sz, ptr, ns + 1, st));
+    MWCG_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, sz + ns + 1, ptr + ns + 1, ns + 1, st));
+    int64_t stored = 0, n_rec = 0;
     unsigned int reject = 0;
-    MWCG_CUDA(cudaMemcpyAsync(&total, slice_ptr + A.n_slices, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    MWCG_CUDA(cudaMemcpyAsync(&stored, ptr + ns, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    MWCG_CUDA(cudaMemcpyAsync(&n_rec, ptr + 2 * ns + 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     MWCG_CUDA(cudaMemcpyAsync(&reject, flag, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
     MWCG_CUDA(cudaStreamSynchronize(st));
     pool_free(tmp, st);
-    pool_free(slice_sz, st);
+    pool_free(sz, st);
     pool_free(flag, st);
+    const int64_t total = n_rec * SLICE;
+    auto drop = [&]() {
+        pool_free(ptr, st);
+        pool_free(info, st);
+    };
     if (!force && (reject || total * 100 > sell_total * 106)) {
-        pool_free(slice_ptr, st);
+        drop();
         return 0;
     }
     if (reject) {
-        pool_free(slice_ptr, st);
-        set_error("slice-shared offsets: a slice needs more than Lmax + %d slots", DIA_SLACK);
+        drop();
+        set_error("slice-shared offsets: a slice needs more than Lmax + %d (or %d) slots", DIA_SLACK,
+                  DIA_MAX_SLOTS);
         return MWCG_ERR_VALUE;
     }
-    const size_t ne = (size_t)(total > 0 ? total : 32);
-    MWCG_CUDA(pool_alloc((void **)&M->om, sizeof(uint64_t) * (ne / 32), st));
+    if ((uint64_t)(stored >> 5) > DIA_START_MASK) {
+        drop();
+        set_error("slice-shared offsets: too many stored values");
+        return MWCG_ERR_VALUE;
+    }
+    ulonglong2 *rec = nullptr;
+    MWCG_CUDA(pool_alloc((void **)&rec, sizeof(ulonglong2) * (size_t)(n_rec > 0 ? n_rec : 1), st));
     // DIA_PAD slots of slack: a chunk of the last slice reads past its end
-    MWCG_CUDA(pool_alloc((void **)&M->vals, sizeof(double) * (ne + DIA_PAD * SLICE), st));
-    MWCG_CUDA(cudaMemsetAsync(M->vals + ne, 0, sizeof(double) * DIA_PAD * SLICE, st));
-    dia_walk_kernel<I, true><<<blocks, 256, 0, st>>>(rp, ci, va, A.n_rows, A.n_slices, A.row_base, nullptr,
-                                                     slice_ptr, M->om, M->vals, nullptr);
+    MWCG_CUDA(pool_alloc((void **)&M->vals, sizeof(double) * ((size_t)stored + DIA_PAD * SLICE), st));
+    MWCG_CUDA(cudaMemsetAsync(M->vals + stored, 0, sizeof(double) * DIA_PAD * SLICE, st));
+    dia_walk_kernel<I, true><<<blocks, 256, 0, st>>>(rp, ci, va, A.n_rows, ns, A.row_base, 0, nullptr, nullptr, info,
+                                                     ptr, ptr + ns + 1, rec, M->vals, nullptr);
     MWCG_CHECK_LAUNCH();
-    int rc = dia_patterns(M, slice_ptr, (int64_t)(ne / 32), st);
+    int rc = dia_patterns(M, ptr, ptr + ns + 1, info, rec, n_rec, st);
+    pool_free(rec, st);
+    drop();
     if (rc) return rc;
-    M->slice_ptr = slice_ptr;
     A.total = total;
+    A.stored = stored;
     A.dia = 1;
     A.col16 = 0;
-    A.slice_ptr = slice_ptr;
+    A.slice_ptr = M->slice_ptr;
     A.cols = nullptr;
     A.vals = M->vals;
-    A.om = M->om;
+    A.pat = M->pat;
     MWCG_CUDA(cudaStreamSynchronize(st));
     return 1;
 }
 
 template <typename I>
 static int build_sell(SellMatrixOwned *M, const I *rp, const I *ci, const double *va, int col_format,
-                      int sigma, cudaStream_t st) {
+                      int sigma, bool uniform, cudaStream_t st) {
     SellMatrix &A = M->view;
     int64_t n_pad = A.n_slices * SLICE;
     int64_t *slice_sz = nullptr;
@@ -317,11 +360,16 @@ static int build_sell(SellMatrixOwned *M, const I *rp, const I *ci, const double
     if (col_format == 2 || col_format < 0) {  // slice-shared offsets when they pay
         const int64_t *sell_ptr = M->slice_ptr;
         M->slice_ptr = nullptr;
-        int rc = build_dia<I>(M, rp, ci, va, total, col_format == 2, st);
+        int rc = build_dia<I>(M, rp, ci, va, total, col_format == 2, uniform, st);
         if (rc == 1) {
             pool_free((void *)sell_ptr, st);
             return 0;
         }
+        pool_free(M->slice_ptr, st);  // a descriptor table of a rejected attempt
+        pool_free(M->vals, st);
+        pool_free(M->pat, st);
+        M->vals = nullptr;
+        M->pat = nullptr;
         M->slice_ptr = (int64_t *)sell_ptr;
         A.total = total;
         if (rc != 0) return rc;
@@ -391,6 +439,7 @@ static int build_sell(SellMatrixOwned *M, const I *rp, const I *ci, const double
         MWCG_CHECK_LAUNCH();
     }
     pool_free(pos_of, st);
+    A.stored = total;
     A.slice_ptr = M->slice_ptr;
     A.cols = M->cols;
     A.vals = M->vals;
@@ -415,8 +464,11 @@ int sell_create(SellMatrixOwned **out, int64_t n_rows, int64_t n_cols, int64_t n
     }
     // flags (include/mwcg_cuda.h): sigma -1 off / 0 auto / 1 forced
     int sigma = 0;
+    bool uniform = true;
+    if (const char *e = getenv("MWCG_DIA_UNIFORM")) uniform = atoi(e) != 0;  // A/B switch (tools/)
     if (col_format >= 0) {
         sigma = (col_format & MWCG_SELL_SIGMA) ? 1 : ((col_format & MWCG_SELL_NO_SIGMA) ? -1 : 0);
+        if (col_format & MWCG_DIA_STREAM_VALUES) uniform = false;
         col_format &= 15;
         if (col_format == 15) col_format = -1;
     }
@@ -428,9 +480,9 @@ int sell_create(SellMatrixOwned **out, int64_t n_rows, int64_t n_cols, int64_t n
     M->view.row_base = row_base;
     int rc = (index_bytes == 8)
                  ? build_sell<int64_t>(M, (const int64_t *)row_ptr, (const int64_t *)col_idx, values,
-                                       col_format, sigma, st)
+                                       col_format, sigma, uniform, st)
                  : build_sell<int32_t>(M, (const int32_t *)row_ptr, (const int32_t *)col_idx, values,
-                                       col_format, sigma, st);
+                                       col_format, sigma, uniform, st);
     if (rc != 0) {
         sell_destroy(M);
         return rc;
@@ -444,7 +496,7 @@ void sell_destroy(SellMatrixOwned *M) {
     pool_free(M->slice_ptr, 0);
     pool_free(M->cols, 0);
     pool_free(M->vals, 0);
-    pool_free(M->om, 0);
+    pool_free(M->pat, 0);
     pool_free(M->perm, 0);
     delete M;
 }

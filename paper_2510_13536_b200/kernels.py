@@ -117,8 +117,8 @@ def device_matrix(A, row_base=0, col_format=-1):
     """SELL-32 device copy of a CsrMatrix, built once and cached on A.
     row_base: global index of row 0 when A holds a rank's rows with global
     columns (dist.py); col_format: -1 auto / 0 int32 / 1 int16 deltas /
-    2 slice-shared offsets, optionally | _lib.SELL_SIGMA / _lib.SELL_NO_SIGMA
-    ("auto" is 15 with a flag) (include/mwcg_cuda.h)."""
+    2 slice-shared offsets, optionally | _lib.SELL_SIGMA / _lib.SELL_NO_SIGMA /
+    _lib.DIA_STREAM_VALUES ("auto" is 15 with a flag) (include/mwcg_cuda.h)."""
     h = getattr(A, "_device", None)
     if h is not None:
         return h
@@ -166,6 +166,11 @@ class _DeviceMatrix:
         out = ctypes.c_int64()
         _lib.check(_lib.load().mwcg_matrix_info(self.handle, None, None, None, ctypes.byref(out)))
         return out.value
+
+    def stored_values(self):
+        """Value entries the layout stores and streams per SpMV (value-uniform
+        slices of the slice-shared layout store none)."""
+        return int(_lib.load().mwcg_matrix_stored_values(self.handle))
 
 
 # ---------------------------------------------------------------- scalars
