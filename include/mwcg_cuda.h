@@ -116,6 +116,12 @@ int mwcg_matrix_create_ex(mwcg_matrix **out, int64_t n_rows, int64_t n_cols, int
                           int index_bytes, int64_t row_base, int col_format, void *stream);
 int mwcg_matrix_col_bytes(const mwcg_matrix *A);   /* 2 (int16 deltas), 4 (int32), 0 (slice-shared) */
 int mwcg_matrix_sigma_sorted(const mwcg_matrix *A); /* 1 if the rows of each tile are length-sorted */
+/* Column blocks: an irregular (int32-SELL) matrix with >= 2^22 columns also
+ * keeps its entries cut into column ranges of 2^21 (MWCG_COLBLOCK=<columns>
+ * overrides, 0 = off); the solver's SpMV walks the ranges in turn, each
+ * row's running sum carried in q, so one pass gathers only a range of p that
+ * fits the L2.  Same additions in the same order: bitwise-identical q. */
+int mwcg_matrix_col_blocks(const mwcg_matrix *A);   /* number of column blocks (0: not blocked) */
 int mwcg_matrix_destroy(mwcg_matrix *A);
 int mwcg_matrix_info(const mwcg_matrix *A, int64_t *n_rows, int64_t *n_cols, int64_t *nnz,
                      int64_t *padded_entries);
@@ -174,7 +180,8 @@ int mwcg_solver_time_k1(mwcg_solver *s, int reps, double *us);
 int mwcg_solver_state(mwcg_solver *s, mwcg_state *out);
 /* Kernel configuration the solver chose (introspection for tests / bench):
  * out[0..3] grid of K1 / K2 / K3 / init, [4] TMA-staged K2, [5] TMA-staged
- * K3, [6] SELL-sigma row order.  n: capacity of out. */
+ * K3, [6] SELL-sigma row order, [7] column blocks K1 walks (0: none).
+ * n: capacity of out. */
 int mwcg_solver_describe(const mwcg_solver *s, int64_t *out, int n);
 /* norm_metrics_tw (kernels.py:305-328) of the current iterate */
 int mwcg_solver_metrics(mwcg_solver *s, double *err, double *true_res);

@@ -131,9 +131,9 @@ class Solver:
 
     def describe(self):
         """The kernel configuration the library chose (mwcg_solver_describe)."""
-        out = (ctypes.c_int64 * 7)()
-        _lib.check(self._L.mwcg_solver_describe(self.handle, out, 7))
-        keys = ("grid_k1", "grid_k2", "grid_k3", "grid_init", "tma_k2", "tma_k3", "sell_sigma")
+        out = (ctypes.c_int64 * 8)()
+        _lib.check(self._L.mwcg_solver_describe(self.handle, out, 8))
+        keys = ("grid_k1", "grid_k2", "grid_k3", "grid_init", "tma_k2", "tma_k3", "sell_sigma", "col_blocks")
         return dict(zip(keys, (int(v) for v in out)))
 
     def solve(self, b_dev, b_norm, x0_dev=None, xs_dev=None, epsilon=1e-12, max_iterations=None,

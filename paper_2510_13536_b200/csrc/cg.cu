@@ -166,6 +166,10 @@ struct Geo {
     // by default, the interior or the boundary set for the overlapped
     // multi-GPU SpMV (mwcg_solver_set_interior)
     int64_t a0, a1, b0, b1;
+    // column-blocked K1 (sell.cu): this launch starts every row from the
+    // running sum left in q by the previous block (acc_in) and / or leaves
+    // its running sum there for the next one (acc_out: no p.q, no scalar step)
+    int acc_in, acc_out;
 };
 __device__ __forceinline__ int64_t k1_count(const Geo &g) { return (g.a1 - g.a0) + (g.b1 - g.b0); }
 __device__ __forceinline__ int64_t k1_tile(const Geo &g, int64_t t) {
@@ -226,6 +230,7 @@ __global__ void __launch_bounds__(SpTraits<M>::THREADS, SpTraits<M>::MINB)
     // length inside the tile: SELL-sigma) stage the terms in shared memory by
     // natural row, and the first 256 threads replay the canonical order
     constexpr bool STAGE = FUSED && (NT != TILE_THREADS || !std::is_same<CT, DiaTag>::value);
+    constexpr bool BLK = std::is_same<CT, int32_t>::value;  // the layout column blocks use
     __shared__ double terms[STAGE ? W * TILE : 1];
     __shared__ double smem[W * TILE_THREADS / 32];
     __shared__ int s_last;
@@ -253,18 +258,27 @@ __global__ void __launch_bounds__(SpTraits<M>::THREADS, SpTraits<M>::MINB)
             const int row = std::is_same<CT, DiaTag>::value ? pos : (int)sell_row(A, pos);
             if (pos < n) {
                 // columns are global: p is the full (replicated) vector
-                V<W> sv = spmv_row<M, SpTraits<M>::U, CT, true, SpTraits<M>::UU>(A, p, 0, pos, sw);
+                V<W> sv;
+                if constexpr (BLK) {
+                    V<W> s0 = zero<W>();
+                    if (g.acc_in) s0 = load<W>(q + row, g.ld, 0);
+                    sv = spmv_row_sell<M, SpTraits<M>::U, CT, true>(A, p, 0, pos, sw, s0);
+                } else {
+                    sv = spmv_row<M, SpTraits<M>::U, CT, true, SpTraits<M>::UU>(A, p, 0, pos, sw);
+                }
                 // the next row's slice words head its dependency chain: their
                 // load is issued here, under this row's p.q term
                 if (more) sw = slice_words<CT>(A, pos + NT);
-                if (norm_all) sv = Ar::norm(sv);
+                if (!BLK || !g.acc_out) {
+                    if (norm_all) sv = Ar::norm(sv);
+                    if (FUSED) term = Ar::mul(load_aos_ro<W>(pl + (int64_t)row * W, 0), sv);
+                    if (FUSED && !STAGE) acc = Ar::add(acc, term);
+                }
                 store<W>(q + row, g.ld, 0, sv);
-                if (FUSED) term = Ar::mul(load_aos_ro<W>(pl + (int64_t)row * W, 0), sv);
-                if (FUSED && !STAGE) acc = Ar::add(acc, term);
             } else if (more) {
                 sw = slice_words<CT>(A, pos + NT);
             }
-            if (STAGE) {
+            if (STAGE && !(BLK && g.acc_out)) {
 #pragma unroll
                 for (int w = 0; w < W; w++) terms[w * TILE + (row & (TILE - 1))] = term.w[w];
             }
@@ -272,6 +286,7 @@ __global__ void __launch_bounds__(SpTraits<M>::THREADS, SpTraits<M>::MINB)
             pos += NT;
         }
         const int tile2 = pos >> 10;
+        if (BLK && g.acc_out) continue;  // grid-uniform: this block only carries the sums
         if (STAGE) {
             __syncthreads();
             if (threadIdx.x < TILE_THREADS) {
@@ -292,7 +307,7 @@ __global__ void __launch_bounds__(SpTraits<M>::THREADS, SpTraits<M>::MINB)
             if (threadIdx.x == 0) store_part<W>(part, g.part_ld, g.tile_off + tile2, acc);
         }
     }
-    if (!FUSED || !g.final_) return;
+    if (!FUSED || !g.final_ || (BLK && g.acc_out)) return;
     if (!last_block_done(&st->ticket[0], &s_last)) return;
     V<W> pq = reduce_partials_first<M>(part, g.part_ld, g.ntiles_glob, smem);
     if (threadIdx.x == 0) {
@@ -865,10 +880,13 @@ using namespace mwcg;
 
 struct mwcg_matrix {
     SellMatrixOwned *M;
+    std::vector<SellMatrixOwned *> blocks;  // column blocks for K1 (sell.cu); empty: none
 };
 
 struct mwcg_solver {
     SellMatrix A{};
+    std::vector<SellMatrix> blocks;      // column blocks of A (K1 walks them in turn); empty: none
+    std::vector<int64_t> block_col0;     // first column of each block (+ n_cols at the end)
     int mode = 0, W = 1;
     mwcg_solver_config cfg{};
     int64_t n = 0, ntiles = 0, parts = 1;
@@ -899,10 +917,21 @@ struct mwcg_solver {
     bool tma = false;                    // TMA-staged K3 (aligned planes; MWCG_TMA=0/1 overrides)
     bool tma2 = false;                   // TMA-staged K2 (MWCG_TMA2=0/1 overrides)
     cudaAccessPolicyWindow l2win{};      // K1's persisting-L2 window over p (num_bytes 0: none)
+    size_t l2_aside = 0;                 // the device's persisting set-aside (bytes)
     int64_t ilo = 0, ihi = 0;            // interior tiles of a rank (SPMV_INTERIOR)
 };
 
 namespace {
+
+void copy_blocks(mwcg_solver *s, const mwcg_matrix *A) {
+    s->blocks.clear();
+    s->block_col0.clear();
+    for (auto *b : A->blocks) {
+        s->blocks.push_back(b->view);
+        s->block_col0.push_back(b->col0);
+    }
+    if (!A->blocks.empty()) s->block_col0.push_back(A->blocks.back()->col1);
+}
 
 // Stage launchers shared by the graph body, the profiled (kernel-by-kernel)
 // loop and the multi-rank driver.  fused: tile-tree dots inside K1/K2;
@@ -928,6 +957,28 @@ void launch_k1(mwcg_solver *s, cudaStream_t st, cudaGraphConditionalHandle h, in
     const double *pc = s->p;
 #define K1_LAUNCH(CT) \
     cudaLaunchKernelEx(&cfg, cg_spmv_pq<M, FUSED, CT>, s->A, pc, s->q, g, s->part, s->st, h, use_cond)
+    const bool whole = g.a0 == 0 && g.a1 == g.ntiles && g.b0 == g.b1;  // not an interior/boundary split
+    if (!s->blocks.empty() && whole) {
+        // column blocks: one launch per block, the row sums carried in q; each
+        // launch pins ITS range of p in L2 (the block is sized to fit)
+        const size_t nblk = s->blocks.size();
+        for (size_t b = 0; b < nblk; b++) {
+            Geo gb = g;
+            gb.acc_in = b > 0;
+            gb.acc_out = b + 1 < nblk;
+            cudaAccessPolicyWindow w = s->l2win;
+            if (w.num_bytes > 0) {
+                const size_t rec = sizeof(double) * (size_t)s->W;
+                w.base_ptr = (void *)(s->p + s->block_col0[b] * s->W);
+                w.num_bytes = (size_t)(s->block_col0[b + 1] - s->block_col0[b]) * rec;
+                w.hitRatio = (float)std::min(1.0, (double)s->l2_aside / (double)w.num_bytes);
+                at[0].val.accessPolicyWindow = w;
+            }
+            cudaLaunchKernelEx(&cfg, cg_spmv_pq<M, FUSED, int32_t>, s->blocks[b], pc, s->q, gb, s->part, s->st, h,
+                               use_cond);
+        }
+        return;
+    }
     if (s->A.dia) K1_LAUNCH(DiaTag);
     else if (s->A.col16) K1_LAUNCH(int16_t);
     else K1_LAUNCH(int32_t);
@@ -1091,6 +1142,7 @@ int compute_grids_t(mwcg_solver *s) {
             size_t cur = 0;
             cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
             const size_t win = std::min(pbytes, (size_t)max_win);
+            s->l2_aside = cur;
             s->l2win.base_ptr = s->p;
             s->l2win.num_bytes = win;
             s->l2win.hitRatio = (float)std::min(1.0, (double)cur / (double)win);
@@ -1253,9 +1305,24 @@ int mwcg_matrix_create_ex(mwcg_matrix **out, int64_t n_rows, int64_t n_cols, int
     int rc = sell_create(&M, n_rows, n_cols, nnz, row_ptr, col_idx, values, index_bytes, row_base, col_format,
                          (cudaStream_t)stream);
     if (rc) return rc;
-    *out = new mwcg_matrix{M};
+    auto *A = new mwcg_matrix{M, {}};
+    // column blocks for K1 (sell.cu): irregular (int32-SELL) matrices whose
+    // gathered vector outgrows the L2.  MWCG_COLBLOCK=<columns per block>
+    // overrides (0: off); default 2^21 columns (a 32-MB range of a DW p) once
+    // the matrix has at least twice as many.
+    int64_t cpb = (n_cols >= ((int64_t)1 << 22)) ? ((int64_t)1 << 21) : 0;
+    if (const char *e = std::getenv("MWCG_COLBLOCK")) cpb = std::atoll(e);
+    rc = sell_colblocks(A->blocks, M, row_ptr, col_idx, values, index_bytes, cpb, (cudaStream_t)stream);
+    if (rc) {
+        sell_destroy(M);
+        delete A;
+        return rc;
+    }
+    *out = A;
     return 0;
 }
+
+int mwcg_matrix_col_blocks(const mwcg_matrix *A) { return A ? (int)A->blocks.size() : -1; }
 
 int mwcg_matrix_sigma_sorted(const mwcg_matrix *A) { return A && A->M->view.perm ? 1 : 0; }
 
@@ -1268,6 +1335,7 @@ int64_t mwcg_matrix_stored_values(const mwcg_matrix *A) { return A ? A->M->view.
 int mwcg_matrix_destroy(mwcg_matrix *A) {
     if (A) {
         sell_destroy(A->M);
+        for (auto *b : A->blocks) sell_destroy(b);
         delete A;
     }
     return 0;
@@ -1315,6 +1383,7 @@ int mwcg_solver_create(mwcg_solver **out, const mwcg_matrix *A, const mwcg_solve
     }
     auto *s = new mwcg_solver();
     s->A = A->M->view;
+    copy_blocks(s, A);
     s->mode = cfg->mode;
     s->W = words_of(cfg->mode);
     s->cfg = *cfg;
@@ -1399,6 +1468,7 @@ int mwcg_solver_create_dist(mwcg_solver **out, const mwcg_matrix *A, const mwcg_
     }
     auto *s = new mwcg_solver();
     s->A = A->M->view;
+    copy_blocks(s, A);
     s->mode = cfg->mode;
     s->W = words_of(cfg->mode);
     s->cfg = *cfg;
@@ -1494,9 +1564,9 @@ int mwcg_solver_describe(const mwcg_solver *s, int64_t *out, int n) {
         set_error("null argument");
         return MWCG_ERR_VALUE;
     }
-    const int64_t v[7] = {s->grid[0], s->grid[1], s->grid[2], s->grid[3], s->tma2 ? 1 : 0, s->tma ? 1 : 0,
-                          s->A.perm ? 1 : 0};
-    for (int i = 0; i < n && i < 7; i++) out[i] = v[i];
+    const int64_t v[8] = {s->grid[0], s->grid[1], s->grid[2], s->grid[3], s->tma2 ? 1 : 0, s->tma ? 1 : 0,
+                          s->A.perm ? 1 : 0, (int64_t)s->blocks.size()};
+    for (int i = 0; i < n && i < 8; i++) out[i] = v[i];
     return 0;
 }
 
@@ -1829,7 +1899,8 @@ int mwcg_cg_solve(mwcg_solver *s, const double *b, double b_norm, const double *
     };
     if ((rc = record(0, stt.rel))) return rc;
     int64_t body_kernels = 0;  // kernels launched by the iteration loop
-    const int per_it = s->fused ? 3 : 7;
+    // column blocks: K1 is one launch per block
+    const int per_it = (s->fused ? 3 : 7) + (s->blocks.empty() ? 0 : (int)s->blocks.size() - 1);
     while (stt.status == RUNNING) {
         const int64_t k_before = stt.k;
         int64_t next = (stt.k / history_stride + 1) * history_stride;

@@ -20,6 +20,7 @@ struct SellMatrixOwned {
     ulonglong2 *pat = nullptr;  // slice-shared-offset pattern table (dia layout)
     uint16_t *perm = nullptr;  // SELL-sigma row permutation (common.cuh: sell_row)
     int64_t n_patterns_words = 0;
+    int64_t col0 = 0, col1 = 0;  // column range when this is one block of a column-blocked matrix
 };
 
 // the dia descriptor table is padded with this many empty slices
@@ -31,6 +32,12 @@ int sell_create(SellMatrixOwned **out, int64_t n_rows, int64_t n_cols, int64_t n
                 const void *row_ptr, const void *col_idx, const double *values, int index_bytes,
                 int64_t row_base, int col_format, cudaStream_t st);
 void sell_destroy(SellMatrixOwned *M);
+// Column blocks of an int32-SELL matrix (sell.cu): `out` stays empty when the
+// layout is banded (slice-shared / int16 deltas), cols_per_block <= 0, or
+// the matrix has at most cols_per_block columns.
+int sell_colblocks(std::vector<SellMatrixOwned *> &out, const SellMatrixOwned *M, const void *row_ptr,
+                   const void *col_idx, const double *values, int index_bytes, int64_t cols_per_block,
+                   cudaStream_t st);
 
 // operator-level launches (ops.cu); all stream-ordered
 int launch_spmv(int mode, const SellMatrix &A, const double *x, int64_t ldx, double *y, int64_t ldy,

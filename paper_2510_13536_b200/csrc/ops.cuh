@@ -6,13 +6,40 @@
 
 namespace mwcg {
 
-// The matrix is streamed once per iteration: its loads carry an evict-first
-// L2 policy (ld.global.cs) so they do not push the multi-word vectors, which
-// the next kernel re-reads, out of the 126 MB L2.
+// The matrix is streamed once per iteration.  Its loads (a) do not allocate
+// in L1 -- the L1 is kept for the gathered vector, whose near-diagonal records
+// are re-read by neighbouring rows -- and (b) carry an evict-first L2 policy,
+// so they do not push the multi-word vectors, which the next kernel re-reads,
+// out of the 126 MB L2.  (MWCG_STREAM_EF: the plain ld.global.cs form.)
+#ifdef MWCG_STREAM_EF
 __device__ __forceinline__ int ld_stream(const int32_t *p) { return __ldcs(p); }
 __device__ __forceinline__ int16_t ld_stream(const int16_t *p) { return __ldcs((const short *)p); }
 __device__ __forceinline__ double ld_stream(const double *p) { return __ldcs(p); }
-
+#else
+__device__ __forceinline__ uint64_t evict_first_policy() {
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ int ld_stream(const int32_t *p) {
+    int v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;"
+                 : "=r"(v) : "l"(p), "l"(evict_first_policy()));
+    return v;
+}
+__device__ __forceinline__ int16_t ld_stream(const int16_t *p) {
+    short v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s16 %0, [%1], %2;"
+                 : "=h"(v) : "l"(p), "l"(evict_first_policy()));
+    return v;
+}
+__device__ __forceinline__ double ld_stream(const double *p) {
+    double v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+                 : "=d"(v) : "l"(p), "l"(evict_first_policy()));
+    return v;
+}
+#endif
 // One SpMV row: y_r = sum_k add(acc, dxmul(a_rk, x_{c_rk})), acc from +0,
 // strictly left to right (spmv_<mode>: _fast.py:284-290, 329-339, 383-393,
 // 443-455, 501-513; kernels.py:175-180).
@@ -199,10 +226,13 @@ __device__ __forceinline__ mw::V<mw::Arith<M>::W> spmv_row_dia(const SellMatrix 
     return s;
 }
 
+// `sum0`: the sum the walk starts from (+0, or the row's running sum when the
+// matrix is one column block of a larger one: sell.cu, column blocks)
 template <int M, int U, typename CT, bool XAOS = false>
 __device__ __forceinline__ mw::V<mw::Arith<M>::W> spmv_row_sell(const SellMatrix &A,
                                                                 const double *__restrict__ x, int64_t ldx,
-                                                                int64_t row, SliceWords sw) {
+                                                                int64_t row, SliceWords sw,
+                                                                mw::V<mw::Arith<M>::W> sum0) {
     using Ar = mw::Arith<M>;
     constexpr int W = Ar::W;
     // `row` is the storage position (slice row); columns decode against the
@@ -213,7 +243,7 @@ __device__ __forceinline__ mw::V<mw::Arith<M>::W> spmv_row_sell(const SellMatrix
     const int grow = (int)(A.row_base + (std::is_same<CT, int16_t>::value ? sell_row(A, row) : row));
     const CT *__restrict__ cp = (const CT *)A.cols + off;
     const double *__restrict__ vp = A.vals + off;
-    mw::V<W> s = mw::zero<W>();
+    mw::V<W> s = sum0;
     for (int k0 = 0; k0 < L; k0 += U) {
         int c[U];
         bool ok[U];
@@ -243,7 +273,7 @@ __device__ __forceinline__ mw::V<mw::Arith<M>::W> spmv_row(const SellMatrix &A,
                                                            const double *__restrict__ x, int64_t ldx,
                                                            int64_t row, SliceWords sw) {
     if constexpr (std::is_same<CT, DiaTag>::value) return spmv_row_dia<M, U, XAOS, UU>(A, x, ldx, row, sw);
-    else return spmv_row_sell<M, U, CT, XAOS>(A, x, ldx, row, sw);
+    else return spmv_row_sell<M, U, CT, XAOS>(A, x, ldx, row, sw, mw::zero<mw::Arith<M>::W>());
 }
 template <int M, int U, typename CT, bool XAOS = false>
 __device__ __forceinline__ mw::V<mw::Arith<M>::W> spmv_row(const SellMatrix &A,

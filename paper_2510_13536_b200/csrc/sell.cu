@@ -491,6 +491,132 @@ int sell_create(SellMatrixOwned **out, int64_t n_rows, int64_t n_cols, int64_t n
     return 0;
 }
 
+// ---------------------------------------------------------------------------
+// Column blocks (irregular matrices whose gathered vector does not fit the
+// L2: BASELINE config 5).  The columns are cut into ranges of `cols_per_block`
+// and each range becomes its own SELL matrix holding, for every row, the run
+// of the row's entries that falls in the range (CSR rows are sorted by
+// column, so the run is contiguous and the runs of successive blocks ARE the
+// row's entries in order).  K1 walks the blocks one after the other with the
+// row's running sum carried in q: the additions and their left-to-right
+// order are those of the unblocked walk -- every bit of q is the same -- but
+// the gathers of one pass touch only cols_per_block records of p, which stay
+// in L2.
+// ---------------------------------------------------------------------------
+template <typename I>
+__global__ void colblock_count_kernel(const I *__restrict__ rp, const I *__restrict__ ci, int64_t n_rows,
+                                      int64_t c0, int64_t c1, int64_t *__restrict__ lo_out,
+                                      int64_t *__restrict__ cnt) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n_rows) return;
+    const int64_t b = rp[r], e = rp[r + 1];
+    auto lower = [&](int64_t key) {  // first k in [b, e) with ci[k] >= key
+        int64_t lo = b, hi = e;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if ((int64_t)ci[mid] < key) lo = mid + 1;
+            else hi = mid;
+        }
+        return lo;
+    };
+    const int64_t k0 = lower(c0), k1 = lower(c1);
+    lo_out[r] = k0;
+    cnt[r] = k1 - k0;
+}
+
+template <typename I>
+__global__ void colblock_fill_kernel(const I *__restrict__ ci, const double *__restrict__ va, int64_t n_rows,
+                                     const int64_t *__restrict__ lo_in, const int64_t *__restrict__ rp_b,
+                                     int32_t *__restrict__ rp32, int32_t *__restrict__ ci_b,
+                                     double *__restrict__ va_b) {
+    // one warp per row
+    const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (r > n_rows) return;
+    if (r == n_rows) {
+        if (lane == 0) rp32[r] = (int32_t)rp_b[r];
+        return;
+    }
+    const int64_t src = lo_in[r], dst = rp_b[r], len = rp_b[r + 1] - dst;
+    if (lane == 0) rp32[r] = (int32_t)dst;
+    for (int64_t k = lane; k < len; k += 32) {
+        ci_b[dst + k] = (int32_t)ci[src + k];
+        va_b[dst + k] = va[src + k];
+    }
+}
+
+template <typename I>
+static int build_colblocks(std::vector<SellMatrixOwned *> &out, const SellMatrix &full, const I *rp, const I *ci,
+                           const double *va, int64_t cols_per_block, cudaStream_t st) {
+    const int64_t n = full.n_rows;
+    const int64_t nb = (full.n_cols + cols_per_block - 1) / cols_per_block;
+    int64_t *lo = nullptr, *cnt = nullptr, *rpb = nullptr;
+    int32_t *rp32 = nullptr;
+    MWCG_CUDA(pool_alloc((void **)&lo, sizeof(int64_t) * (n + 1), st));
+    MWCG_CUDA(pool_alloc((void **)&cnt, sizeof(int64_t) * (n + 1), st));
+    MWCG_CUDA(pool_alloc((void **)&rpb, sizeof(int64_t) * (n + 1), st));
+    MWCG_CUDA(pool_alloc((void **)&rp32, sizeof(int32_t) * (n + 1), st));
+    size_t tmp_bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt, rpb, n + 1, st);
+    void *tmp = nullptr;
+    MWCG_CUDA(pool_alloc(&tmp, tmp_bytes, st));
+    int rc = 0;
+    for (int64_t b = 0; b < nb && rc == 0; b++) {
+        const int64_t c0 = b * cols_per_block, c1 = std::min(full.n_cols, c0 + cols_per_block);
+        MWCG_CUDA(cudaMemsetAsync(cnt + n, 0, sizeof(int64_t), st));
+        colblock_count_kernel<I><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(rp, ci, n, c0, c1, lo, cnt);
+        MWCG_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, rpb, n + 1, st));
+        int64_t nnz_b = 0;
+        MWCG_CUDA(cudaMemcpyAsync(&nnz_b, rpb + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        MWCG_CUDA(cudaStreamSynchronize(st));
+        if (nnz_b > INT32_MAX) {
+            set_error("column block with more than 2^31-1 entries");
+            rc = MWCG_ERR_VALUE;
+            break;
+        }
+        int32_t *ci_b = nullptr;
+        double *va_b = nullptr;
+        MWCG_CUDA(pool_alloc((void **)&ci_b, sizeof(int32_t) * (size_t)std::max<int64_t>(nnz_b, 1), st));
+        MWCG_CUDA(pool_alloc((void **)&va_b, sizeof(double) * (size_t)std::max<int64_t>(nnz_b, 1), st));
+        colblock_fill_kernel<I><<<(unsigned)(((n + 1) * 32 + 255) / 256), 256, 0, st>>>(ci, va, n, lo, rpb, rp32, ci_b,
+                                                                                      va_b);
+        SellMatrixOwned *Mb = nullptr;
+        // int32 columns, SELL-sigma when it pays (block rows are short and ragged)
+        rc = sell_create(&Mb, n, full.n_cols, nnz_b, rp32, ci_b, va_b, 4, full.row_base, 0, st);
+        pool_free(ci_b, st);
+        pool_free(va_b, st);
+        if (rc == 0) {
+            Mb->col0 = c0;
+            Mb->col1 = c1;
+            out.push_back(Mb);
+        }
+    }
+    MWCG_CUDA(cudaStreamSynchronize(st));
+    pool_free(tmp, st);
+    pool_free(lo, st);
+    pool_free(cnt, st);
+    pool_free(rpb, st);
+    pool_free(rp32, st);
+    if (rc) {
+        for (auto *b : out) sell_destroy(b);
+        out.clear();
+    }
+    return rc;
+}
+
+int sell_colblocks(std::vector<SellMatrixOwned *> &out, const SellMatrixOwned *M, const void *row_ptr,
+                   const void *col_idx, const double *values, int index_bytes, int64_t cols_per_block,
+                   cudaStream_t st) {
+    out.clear();
+    const SellMatrix &A = M->view;
+    if (cols_per_block <= 0 || A.dia || A.col16 || A.n_rows == 0 || A.n_cols <= cols_per_block) return 0;
+    return index_bytes == 8
+               ? build_colblocks<int64_t>(out, A, (const int64_t *)row_ptr, (const int64_t *)col_idx, values,
+                                          cols_per_block, st)
+               : build_colblocks<int32_t>(out, A, (const int32_t *)row_ptr, (const int32_t *)col_idx, values,
+                                          cols_per_block, st);
+}
+
 void sell_destroy(SellMatrixOwned *M) {
     if (!M) return;
     pool_free(M->slice_ptr, 0);

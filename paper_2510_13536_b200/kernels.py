@@ -167,6 +167,10 @@ class _DeviceMatrix:
         _lib.check(_lib.load().mwcg_matrix_info(self.handle, None, None, None, ctypes.byref(out)))
         return out.value
 
+    def col_blocks(self):
+        """Number of column blocks K1 walks (0: the matrix is not blocked)."""
+        return int(_lib.load().mwcg_matrix_col_blocks(self.handle))
+
     def stored_values(self):
         """Value entries the layout stores and streams per SpMV (value-uniform
         slices of the slice-shared layout store none)."""
