@@ -391,7 +391,10 @@ def run_ours(a):
     cb = dmat.col_bytes()
     layout = {"format": {0: "slice-shared offsets (SELL-32 slices, pattern table)", 2: "SELL-32 int16 deltas",
                          4: "SELL-32 int32"}[cb],
-              "col_bytes_per_entry": cb, "padded_entries": dmat.padded_entries(), "nnz": nnz}
+              "col_bytes_per_entry": cb, "padded_entries": dmat.padded_entries(), "nnz": nnz,
+              # value entries K1 actually streams: value-uniform slices keep their
+              # values in the (L1-resident) pattern records (0 for C1/C2)
+              "stored_values": dmat.stored_values(), "col_blocks": dmat.col_blocks()}
     with ClockSampler(local) as clk:
         for _ in range(max(3, a.warmup)):
             device_solve(solver)
@@ -434,6 +437,10 @@ def run_ours(a):
         pass
     roofline = {"bound": "hbm", "achieved": k1_achieved, "peak": hbm, "unit": "GB/s",
                 "frac": k1_achieved / hbm, "traffic": traffic,
+                "traffic_source": prof.get("source"),
+                "traffic_note": "achieved/frac use the ALGORITHMIC (canonical CSR) bytes; traffic is the DRAM "
+                                "bytes ncu measured per launch -- below the algorithmic bytes when the layout "
+                                "streams no column indices / no values for value-uniform slices",
                 "kernel": "cg_spmv_pq (SpMV + fused p.q + alpha)",
                 "algorithmic_bytes_per_launch": k1_bytes(n, nnz, w),
                 "launch_us": k1_launch_s * 1e6, "peak_source": hbm_src,

@@ -16,6 +16,9 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libmwcg_cuda.so")
+# debug build with device-side index checks on every matrix walk (-DMWCG_BOUNDS;
+# csrc/common.cuh), loaded by tests/test_gpu_bounds.py through MWCG_LIB
+LIB_BOUNDS = os.path.join(PKG, "libmwcg_cuda_bounds.so")
 SOURCES = ["capi.cu", "sell.cu", "ops.cu", "cg.cu", "mm.cu", "problemgen.cu"]
 
 NVCC_FLAGS = [
@@ -52,12 +55,25 @@ def build(verbose=False, force=False, defines=(), out=None):
     return lib
 
 
+def build_all(verbose=False, force=False):
+    """The product library and the bounds-checked debug build, compiled side by side."""
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(2) as ex:
+        f1 = ex.submit(build, verbose, force)
+        f2 = ex.submit(build, False, force, ("MWCG_BOUNDS",), LIB_BOUNDS)
+        return f1.result(), f2.result()
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--verbose", action="store_true")
     ap.add_argument("--force", action="store_true")
     ap.add_argument("-D", dest="defines", action="append", default=[])
     ap.add_argument("--out", default=None)
+    ap.add_argument("--all", action="store_true", help="also build the -DMWCG_BOUNDS debug library")
     a = ap.parse_args()
+    if a.all:
+        print(*build_all(verbose=a.verbose, force=a.force or a.verbose))
+        sys.exit(0)
     print(build(verbose=a.verbose, force=a.force or a.verbose, defines=a.defines, out=a.out))
     sys.exit(0)

@@ -269,6 +269,7 @@ __global__ void __launch_bounds__(SpTraits<M>::THREADS, SpTraits<M>::MINB)
                 // the next row's slice words head its dependency chain: their
                 // load is issued here, under this row's p.q term
                 if (more) sw = slice_words<CT>(A, pos + NT);
+                MWCG_ASSERT(row >= 0 && row < n && (row >> 10) == (pos >> 10));
                 if (!BLK || !g.acc_out) {
                     if (norm_all) sv = Ar::norm(sv);
                     if (FUSED) term = Ar::mul(load_aos_ro<W>(pl + (int64_t)row * W, 0), sv);

@@ -69,7 +69,24 @@ struct SellMatrix {
                             // per slice: {start/32 | L << 40 | uniform << 48, pattern base}
     const uint16_t *perm;   // SELL-sigma: storage position -> row within its 1024-row tile
                             // (rows of a tile sorted by length; nullptr: identity)
+    int64_t pat_len;        // dia: records in the pattern table (bounds checks)
 };
+
+// Debug build (-DMWCG_BOUNDS, libmwcg_cuda_bounds.so): every index the matrix
+// walks form -- pattern record, value slot, gathered column -- is checked on the
+// device and a violation traps (compute-sanitizer is not available on every
+// pool; tests/test_gpu_bounds.py runs the layouts through this build).
+#ifdef MWCG_BOUNDS
+#define MWCG_ASSERT(cond)                                                           \
+    do {                                                                            \
+        if (!(cond)) {                                                              \
+            printf("MWCG_BOUNDS %s:%d: %s\n", __FILE__, __LINE__, #cond);           \
+            __trap();                                                               \
+        }                                                                           \
+    } while (0)
+#else
+#define MWCG_ASSERT(cond) ((void)0)
+#endif
 
 // Natural row of storage position `pos` (SELL-sigma permutes rows inside
 // their tile only, so tiles and the canonical tile order are unchanged).

@@ -148,7 +148,7 @@ __device__ __forceinline__ mw::V<W> keep_if(bool ok, mw::V<W> t, mw::V<W> s) {
 template <int M, int N, bool XAOS, bool UNIFORM>
 __device__ __forceinline__ void dia_chunk(mw::V<mw::Arith<M>::W> &s, const ulonglong2 *__restrict__ op,
                                           const double *__restrict__ vp, const double *__restrict__ xg,
-                                          int64_t ldx, uint32_t lbit) {
+                                          int64_t ldx, uint32_t lbit, const SellMatrix &A, int64_t grow) {
     using Ar = mw::Arith<M>;
     constexpr int W = Ar::W;
     double a[N];
@@ -157,6 +157,8 @@ __device__ __forceinline__ void dia_chunk(mw::V<mw::Arith<M>::W> &s, const ulong
 #pragma unroll
     for (int u = 0; u < N; u++) {
         uint64_t om;
+        MWCG_ASSERT(op + u >= A.pat && op + u < A.pat + A.pat_len);
+        MWCG_ASSERT(UNIFORM || (vp + u * SLICE >= A.vals && vp + u * SLICE < A.vals + A.stored + DIA_PAD * SLICE));
         if (UNIFORM) {
             const ulonglong2 rec = __ldg(op + u);
             om = rec.x;
@@ -166,6 +168,7 @@ __device__ __forceinline__ void dia_chunk(mw::V<mw::Arith<M>::W> &s, const ulong
             a[u] = ld_stream(vp + u * SLICE);
         }
         ok[u] = ((uint32_t)(om >> 32) & lbit) != 0;
+        MWCG_ASSERT(!ok[u] || (grow + (int)(uint32_t)om >= 0 && grow + (int)(uint32_t)om < A.n_cols));
         xv[u] = dia_gather<W, XAOS>(xg, ldx, ok[u] ? (int)(uint32_t)om : 0);
     }
     // streamed TW/QTW rows keep the lane branch (C4 QTW K1: 78 us against
@@ -185,20 +188,20 @@ __device__ __forceinline__ void dia_chunk(mw::V<mw::Arith<M>::W> &s, const ulong
 template <int M, int U, bool XAOS, bool UNIFORM>
 __device__ __forceinline__ void dia_walk(mw::V<mw::Arith<M>::W> &s, int L, const ulonglong2 *__restrict__ op,
                                          const double *__restrict__ vp, const double *__restrict__ xg,
-                                         int64_t ldx, uint32_t lbit) {
+                                         int64_t ldx, uint32_t lbit, const SellMatrix &A, int64_t grow) {
     int k0 = 0;
-    for (; k0 + U <= L; k0 += U, op += U, vp += U * SLICE) dia_chunk<M, U, XAOS, UNIFORM>(s, op, vp, xg, ldx, lbit);
+    for (; k0 + U <= L; k0 += U, op += U, vp += U * SLICE) dia_chunk<M, U, XAOS, UNIFORM>(s, op, vp, xg, ldx, lbit, A, grow);
     const int rem = L - k0;
-    if (U > 1 && rem == 1) dia_chunk<M, 1, XAOS, UNIFORM>(s, op, vp, xg, ldx, lbit);
-    if (U > 2 && rem == 2) dia_chunk<M, 2, XAOS, UNIFORM>(s, op, vp, xg, ldx, lbit);
-    if (U > 3 && rem == 3) dia_chunk<M, 3, XAOS, UNIFORM>(s, op, vp, xg, ldx, lbit);
+    if (U > 1 && rem == 1) dia_chunk<M, 1, XAOS, UNIFORM>(s, op, vp, xg, ldx, lbit, A, grow);
+    if (U > 2 && rem == 2) dia_chunk<M, 2, XAOS, UNIFORM>(s, op, vp, xg, ldx, lbit, A, grow);
+    if (U > 3 && rem == 3) dia_chunk<M, 3, XAOS, UNIFORM>(s, op, vp, xg, ldx, lbit, A, grow);
     if (U > 4 && rem >= 4) {  // U up to 8: 4 + (rem - 4)
-        dia_chunk<M, 4, XAOS, UNIFORM>(s, op, vp, xg, ldx, lbit);
+        dia_chunk<M, 4, XAOS, UNIFORM>(s, op, vp, xg, ldx, lbit, A, grow);
         op += 4;
         vp += 4 * SLICE;
-        if (rem == 5) dia_chunk<M, 1, XAOS, UNIFORM>(s, op, vp, xg, ldx, lbit);
-        if (rem == 6) dia_chunk<M, 2, XAOS, UNIFORM>(s, op, vp, xg, ldx, lbit);
-        if (rem == 7) dia_chunk<M, 3, XAOS, UNIFORM>(s, op, vp, xg, ldx, lbit);
+        if (rem == 5) dia_chunk<M, 1, XAOS, UNIFORM>(s, op, vp, xg, ldx, lbit, A, grow);
+        if (rem == 6) dia_chunk<M, 2, XAOS, UNIFORM>(s, op, vp, xg, ldx, lbit, A, grow);
+        if (rem == 7) dia_chunk<M, 3, XAOS, UNIFORM>(s, op, vp, xg, ldx, lbit, A, grow);
     }
 }
 
@@ -212,16 +215,17 @@ __device__ __forceinline__ mw::V<mw::Arith<M>::W> spmv_row_dia(const SellMatrix 
     const uint64_t d0 = (uint64_t)sw.w0;
     const int L = (int)((uint32_t)(d0 >> DIA_LBITS) & 0xffu);
     const bool uniform = ((uint32_t)(d0 >> DIA_LBITS) & 0x100u) != 0;
+    MWCG_ASSERT(A.row_base + row < A.n_cols && sw.w1 >= 0 && sw.w1 + L <= A.pat_len);
     const uint32_t lbit = 1u << ((int)row & 31);
     // the row's own element: every gather is this address + a slot offset
     const double *__restrict__ xg = x + (A.row_base + row) * (XAOS ? W : 1);
     const ulonglong2 *__restrict__ op = A.pat + sw.w1;
     mw::V<W> s = mw::zero<W>();
     if (uniform) {
-        dia_walk<M, UU, XAOS, true>(s, L, op, nullptr, xg, ldx, lbit);
+        dia_walk<M, UU, XAOS, true>(s, L, op, nullptr, xg, ldx, lbit, A, A.row_base + row);
     } else {
         const double *__restrict__ vp = A.vals + (((int64_t)(d0 & DIA_START_MASK) << 5) + ((int)row & 31));
-        dia_walk<M, U, XAOS, false>(s, L, op, vp, xg, ldx, lbit);
+        dia_walk<M, U, XAOS, false>(s, L, op, vp, xg, ldx, lbit, A, A.row_base + row);
     }
     return s;
 }
@@ -251,10 +255,12 @@ __device__ __forceinline__ mw::V<mw::Arith<M>::W> spmv_row_sell(const SellMatrix
 #pragma unroll
         for (int u = 0; u < U; u++) {
             const int64_t kk = min(k0 + u, L - 1);
+            MWCG_ASSERT(off + kk * SLICE >= 0 && off + kk * SLICE < A.total);
             const CT d = ld_stream(cp + kk * SLICE);
             a[u] = ld_stream(vp + kk * SLICE);
             ok[u] = (k0 + u < L) && (d != ColCodec<CT>::SENT);
             c[u] = ok[u] ? ColCodec<CT>::col(grow, d) : 0;
+            MWCG_ASSERT(c[u] >= 0 && c[u] < A.n_cols);
         }
         mw::V<W> xv[U];
 #pragma unroll

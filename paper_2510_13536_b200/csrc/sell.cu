@@ -320,6 +320,7 @@ static int build_dia(SellMatrixOwned *M, const I *rp, const I *ci, const double 
     A.cols = nullptr;
     A.vals = M->vals;
     A.pat = M->pat;
+    A.pat_len = M->n_patterns_words;
     MWCG_CUDA(cudaStreamSynchronize(st));
     return 1;
 }
