@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(SpTraits<M>::THREADS, SpTraits<M>::MINB)
     constexpr bool STAGE = FUSED && (NT != TILE_THREADS || !std::is_same<CT, DiaTag>::value);
     constexpr bool BLK = std::is_same<CT, int32_t>::value;  // the layout column blocks use
     __shared__ double terms[STAGE ? W * TILE : 1];
-    __shared__ double smem[W * TILE_THREADS / 32];
+    __shared__ double smem[tree_smem<W>()];
     __shared__ int s_last;
     if (stopped_k1(st, h, use_cond)) return;
     const bool norm_all = st->norm_all != 0;
@@ -351,7 +351,7 @@ __global__ void __launch_bounds__(TILE_THREADS, Hoist<M>::MINB)
     using Ar = Arith<M>;
     constexpr int W = Ar::W;
     constexpr int H = Hoist<M>::value;
-    __shared__ double smem[W * TILE_THREADS / 32];
+    __shared__ double smem[tree_smem<W>()];
     __shared__ int s_last;
     if (stopped(st, h, use_cond)) return;
     const bool norm_r = st->norm_r != 0;
@@ -571,7 +571,7 @@ __global__ void __launch_bounds__(TILE_THREADS, UpTma<M>::MINB)
     constexpr int W = Ar::W;
     extern __shared__ __align__(128) double ring[];
     __shared__ uint64_t bar[T::NS];
-    __shared__ double smem[W * TILE_THREADS / 32];
+    __shared__ double smem[tree_smem<W>()];
     __shared__ int s_last;
     if (stopped(st, h, use_cond)) return;
     const bool norm_r = st->norm_r != 0;
@@ -722,7 +722,7 @@ __global__ void __launch_bounds__(TILE_THREADS)
             double *__restrict__ p, Geo g, double *__restrict__ part, CgState *st) {
     using Ar = Arith<M>;
     constexpr int W = Ar::W;
-    __shared__ double smem[W * TILE_THREADS / 32];
+    __shared__ double smem[tree_smem<W>()];
     __shared__ int s_last;
     const bool norm_r = st->norm_r != 0;
     const int64_t n = g.n, ld = g.ld;
@@ -787,7 +787,7 @@ __global__ void __launch_bounds__(TILE_THREADS)
     cg_finalize(const double *__restrict__ part, Geo g, CgState *st, int phase) {
     using Ar = Arith<M>;
     constexpr int W = Ar::W;
-    __shared__ double smem[W * TILE_THREADS / 32];
+    __shared__ double smem[tree_smem<W>()];
     if (phase != 0 && halted(st)) return;
     V<W> v = reduce_partials_block<M>(part, g.part_ld, g.ntiles_glob, smem);
     if (threadIdx.x == 0) {

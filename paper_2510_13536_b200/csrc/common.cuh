@@ -142,6 +142,91 @@ __device__ __forceinline__ mw::V<mw::Arith<M>::W> warp_tree(mw::V<mw::Arith<M>::
     return v;
 }
 
+// The SAME tree with every addition executed once: the 256 leaves go through
+// shared memory, level 1 (128 additions) runs on 4 warps, level 2 (64) on 2,
+// and warp 0 finishes levels 3-5 and the three cross-warp levels with
+// shuffles -- 12 warp-level additions per tile instead of 43 (each of the 8
+// warps running the 5-level shuffle tree, then warp 0's 3 levels).  Pairings
+// and operand order are those of warp_tree + the cross-warp stage above, so
+// every bit of the result is unchanged; what changes is the issue and
+// FP64-pipe load of the tile reductions (a third of K2's instruction stream).
+// smem: tree_smem<W>() doubles.  Every thread of the block must call it; the
+// first TILE_THREADS threads hold the leaves.  Result valid in thread 0.
+template <int W>
+__host__ __device__ constexpr int tree_smem() {
+    return W * (TILE_THREADS + TILE_THREADS / 2 + TILE_THREADS / 4);
+}
+
+template <int M>
+__device__ __forceinline__ mw::V<mw::Arith<M>::W> dense_tree(mw::V<mw::Arith<M>::W> v, double *smem) {
+    using A = mw::Arith<M>;
+    constexpr int W = A::W;
+    static_assert(TILE_THREADS == 256, "the level split below is written for 8 warps");
+    double *s0 = smem, *s1 = smem + W * 256, *s2 = s1 + W * 128;
+    const int t = threadIdx.x;
+    if (t < 256) {
+#pragma unroll
+        for (int k = 0; k < W; k++) s0[k * 256 + t] = v.w[k];
+    }
+    __syncthreads();
+    if (t < 128) {  // level 1: leaf (w, l) + leaf (w, l + 16), l < 16; result index w*16 + l == t
+        const int i = (t >> 4) * 32 + (t & 15);
+        mw::V<W> a, b;
+#pragma unroll
+        for (int k = 0; k < W; k++) {
+            a.w[k] = s0[k * 256 + i];
+            b.w[k] = s0[k * 256 + i + 16];
+        }
+        a = A::add(a, b);
+#pragma unroll
+        for (int k = 0; k < W; k++) s1[k * 128 + t] = a.w[k];
+    }
+    __syncthreads();
+    if (t < 64) {  // level 2: (w, l) + (w, l + 8), l < 8; result index w*8 + l == t
+        const int i = (t >> 3) * 16 + (t & 7);
+        mw::V<W> a, b;
+#pragma unroll
+        for (int k = 0; k < W; k++) {
+            a.w[k] = s1[k * 128 + i];
+            b.w[k] = s1[k * 128 + i + 8];
+        }
+        a = A::add(a, b);
+#pragma unroll
+        for (int k = 0; k < W; k++) s2[k * 64 + t] = a.w[k];
+    }
+    __syncthreads();
+    if (t < 32) {  // lane = w*4 + l
+        const int i = (t >> 2) * 8 + (t & 3);
+        mw::V<W> a, b;
+#pragma unroll
+        for (int k = 0; k < W; k++) {
+            a.w[k] = s2[k * 64 + i];
+            b.w[k] = s2[k * 64 + i + 4];
+        }
+        a = A::add(a, b);                            // level 3: (w, l) + (w, l + 4), l < 4
+        a = A::add(a, mw::shfl_down<W>(a, 2));       // level 4: l < 2
+        a = A::add(a, mw::shfl_down<W>(a, 1));       // level 5: warp w's sum at lane 4w
+        a = A::add(a, mw::shfl_down<W>(a, 16));      // cross-warp: w + (w + 4)
+        a = A::add(a, mw::shfl_down<W>(a, 8));       //             w + (w + 2)
+        a = A::add(a, mw::shfl_down<W>(a, 4));       //             w + (w + 1)
+        v = a;
+    }
+    __syncthreads();
+    return v;
+}
+
+#ifndef MWCG_TREE_SHUFFLE
+template <int M, int NT>
+__device__ __forceinline__ mw::V<mw::Arith<M>::W> block_tree(mw::V<mw::Arith<M>::W> v, double *smem) {
+    static_assert(NT == TILE_THREADS, "tile tree");
+    return dense_tree<M>(v, smem);
+}
+template <int M, int NT>
+__device__ __forceinline__ mw::V<mw::Arith<M>::W> block_tree_first(mw::V<mw::Arith<M>::W> v, double *smem) {
+    static_assert(NT == TILE_THREADS, "tile tree");
+    return dense_tree<M>(v, smem);
+}
+#else
 template <int M, int NT>
 __device__ __forceinline__ mw::V<mw::Arith<M>::W> block_tree(mw::V<mw::Arith<M>::W> v,
                                                              double *smem /* W*NT/32 */) {
@@ -205,6 +290,8 @@ __device__ __forceinline__ mw::V<mw::Arith<M>::W> block_tree_first(mw::V<mw::Ari
     __syncthreads();
     return v;
 }
+
+#endif  // MWCG_TREE_SHUFFLE
 
 // Tile-partial layout: rank-blocked word planes.  Word k of global tile t
 // lives at part[(t / tb) * (W * tb) + k * tb + t % tb]: the tiles of one rank

@@ -31,7 +31,7 @@ __global__ void __launch_bounds__(TILE_THREADS) dot_tile_kernel(int64_t n, const
                                                                 double *__restrict__ out) {
     using Ar = Arith<M>;
     constexpr int W = Ar::W;
-    __shared__ double smem[W * TILE_THREADS / 32];
+    __shared__ double smem[tree_smem<W>()];
     __shared__ int s_last;
     V<W> acc = zero<W>();
     const int64_t base = (int64_t)blockIdx.x * TILE + threadIdx.x;
