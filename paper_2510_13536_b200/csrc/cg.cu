@@ -1692,6 +1692,12 @@ int mwcg_solver_time_k1(mwcg_solver *s, int reps, double *us) {
     MWCG_CUDA(cudaMemcpyAsync(&s->st->k_stop, s->kstop_host, sizeof(long long), cudaMemcpyHostToDevice, st));
     MWCG_CUDA(cudaMemsetAsync(&s->st->pause, 0, sizeof(int), st));
     cudaGraphConditionalHandle h{};
+    // MWCG_NOTAIL=1 (tools/): time K1 without its serial tail (the last CTA's
+    // reduction of the partials and the scalar step) -- a diagnostic, results unused
+    const int final_saved = s->geo.final_;
+    if (const char *e = std::getenv("MWCG_NOTAIL")) {
+        if (std::atoi(e) != 0) s->geo.final_ = 0;
+    }
     for (int pass = 0; pass < 2; pass++) {  // pass 0 warms up
         MWCG_CUDA(cudaEventRecord(s->ev[6], st));
         for (int r = 0; r < reps; r++) {
@@ -1707,6 +1713,7 @@ int mwcg_solver_time_k1(mwcg_solver *s, int reps, double *us) {
         MWCG_CUDA(cudaEventRecord(s->ev[7], st));
         MWCG_CUDA(cudaEventSynchronize(s->ev[7]));
     }
+    s->geo.final_ = final_saved;
     float ms = 0.f;
     MWCG_CUDA(cudaEventElapsedTime(&ms, s->ev[6], s->ev[7]));
     *us = 1e3 * (double)ms / reps;

@@ -157,10 +157,28 @@ __host__ __device__ constexpr int tree_smem() {
     return W * (TILE_THREADS + TILE_THREADS / 2 + TILE_THREADS / 4);
 }
 
-template <int M>
+// COLD: the copy that runs ONCE per kernel, in the last CTA's reduction of the
+// tile partials.  That serial tail executes each instruction once, so its time
+// is instruction fetch, and for TW -- 204 instructions per addition -- the fully
+// inlined tail was ~4000 straight-line instructions during which every other SM
+// sat idle (ncu, C2 TW: 41 % of K2's and ~20 % of K1's elapsed cycles had no
+// resident warp outside that one CTA; profiles/r2v_ncu_k23_tw.json).  The cold
+// copy calls ONE out-of-line tw_add (mw::add_cold) instead: TW 451 -> 391 us/it.
+// The cheap additions of the other modes stay inline (calls and rolled loops
+// cost them 4-6 us/it: profiles/r2w_*.json).
+template <int M, bool COLD>
+struct TailAdd {
+    static __device__ __forceinline__ mw::V<mw::Arith<M>::W> add(mw::V<mw::Arith<M>::W> a,
+                                                                 mw::V<mw::Arith<M>::W> b) {
+        if constexpr (COLD && M == mw::TW) return mw::add_cold<M>(a, b);
+        else return mw::Arith<M>::add(a, b);
+    }
+};
+
+template <int M, bool COLD = false>
 __device__ __forceinline__ mw::V<mw::Arith<M>::W> dense_tree(mw::V<mw::Arith<M>::W> v, double *smem) {
-    using A = mw::Arith<M>;
-    constexpr int W = A::W;
+    using A = TailAdd<M, COLD>;
+    constexpr int W = mw::Arith<M>::W;
     static_assert(TILE_THREADS == 256, "the level split below is written for 8 warps");
     double *s0 = smem, *s1 = smem + W * 256, *s2 = s1 + W * 128;
     const int t = threadIdx.x;
@@ -316,8 +334,8 @@ __device__ __forceinline__ void store_part(double *part, int64_t tb, int64_t t, 
 template <int M>
 __device__ __forceinline__ mw::V<mw::Arith<M>::W> accumulate_partials(const double *part, int64_t ld,
                                                                       int64_t ntiles) {
-    using A = mw::Arith<M>;
-    constexpr int W = A::W;
+    using A = TailAdd<M, true>;
+    constexpr int W = mw::Arith<M>::W;
     constexpr int PF = 8;
     mw::V<W> acc = mw::zero<W>();
     for (int64_t b = threadIdx.x; b < ntiles; b += (int64_t)PF * TILE_THREADS) {
@@ -342,7 +360,7 @@ __device__ __forceinline__ mw::V<mw::Arith<M>::W> reduce_partials_first(const do
     constexpr int W = A::W;
     mw::V<W> acc = mw::zero<W>();
     if (threadIdx.x < TILE_THREADS) acc = accumulate_partials<M>(part, ld, ntiles);
-    return block_tree_first<M, TILE_THREADS>(acc, smem);
+    return dense_tree<M, true>(acc, smem);
 }
 
 // Second pass over ntiles partials (layout above, tile block ld) by one block of
@@ -351,7 +369,7 @@ __device__ __forceinline__ mw::V<mw::Arith<M>::W> reduce_partials_first(const do
 template <int M>
 __device__ __forceinline__ mw::V<mw::Arith<M>::W> reduce_partials_block(const double *part, int64_t ld,
                                                                          int64_t ntiles, double *smem) {
-    return block_tree<M, TILE_THREADS>(accumulate_partials<M>(part, ld, ntiles), smem);
+    return dense_tree<M, true>(accumulate_partials<M>(part, ld, ntiles), smem);
 }
 
 // Last-block-done election: returns true in every thread of the block that

@@ -311,6 +311,16 @@ MWI V<3> dxtw_add(double a, V<3> b) {
 }
 
 // ------------------------------------------------------------ division
+// Division runs once per dot product, on one thread, in the serial tail of a
+// kernel (the scalar step of K1 / K2): what matters there is the size of the
+// straight-line code, not its instruction count -- cold instruction fetches of
+// a fully inlined tw_div (4 x (dxtw_mul + tw_add) = ~1500 instructions executed
+// once) cost more than the arithmetic.  tw_div's loop is therefore kept rolled
+// and the TW operations it calls are single out-of-line copies.
+#define MWNI static __device__ __noinline__
+MWNI V<3> tw_add_ni(V<3> a, V<3> b) { return tw_add(a, b); }
+MWNI V<3> dxtw_mul_ni(double a, V<3> b) { return dxtw_mul(a, b); }
+
 // dw_div: multiword.py:370-382 (normalized ops, also used for QDW 408)
 MWI V<2> dw_div(V<2> a, V<2> b) {
     V<2> bn = norm_dw(b);
@@ -329,8 +339,11 @@ MWI V<2> dw_div(V<2> a, V<2> b) {
     V<3> c = vseb<3, 2>(e);
     return V<2>{{c.w[0], c.w[1]}};
 }
-// tw_div: multiword.py:385-397, _strict_normalize_tw 400-402
-MWI V<3> tw_div(V<3> a, V<3> b) {
+// tw_div: multiword.py:385-397, _strict_normalize_tw 400-402.  COMPACT (TW): the
+// rolled loop over out-of-line copies; QTW keeps the inlined form (its tail is
+// short enough to stay resident: compact costs it 1.5-3 us/it).
+template <bool COMPACT>
+MWI V<3> tw_div_t(V<3> a, V<3> b) {
     double bz[3] = {b.w[0], b.w[1], b.w[2]}, be[3];
     vec_sum<3>(bz, be);
     V<3> bn = vseb<3, 3>(be);
@@ -339,16 +352,26 @@ MWI V<3> tw_div(V<3> a, V<3> b) {
         return V<3>{{__ddiv_rn(__dadd_rn(__dadd_rn(a.w[0], a.w[1]), a.w[2]), bc), 0.0, 0.0}};
     V<3> r = a;
     double q[4];
+    if constexpr (COMPACT) {
+#pragma unroll 1
+        for (int i = 0; i < 4; i++) {
+            q[i] = __ddiv_rn(r.w[0], bn.w[0]);
+            V<3> t = dxtw_mul_ni(q[i], bn);
+            r = tw_add_ni(r, V<3>{{-t.w[0], -t.w[1], -t.w[2]}});
+        }
+    } else {
 #pragma unroll
-    for (int i = 0; i < 4; i++) {
-        q[i] = __ddiv_rn(r.w[0], bn.w[0]);
-        V<3> t = dxtw_mul(q[i], bn);
-        r = tw_add(r, V<3>{{-t.w[0], -t.w[1], -t.w[2]}});
+        for (int i = 0; i < 4; i++) {
+            q[i] = __ddiv_rn(r.w[0], bn.w[0]);
+            V<3> t = dxtw_mul(q[i], bn);
+            r = tw_add(r, V<3>{{-t.w[0], -t.w[1], -t.w[2]}});
+        }
     }
     double e[4];
     vec_sum<4>(q, e);
     return vseb<4, 3>(e);
 }
+MWI V<3> tw_div(V<3> a, V<3> b) { return tw_div_t<false>(a, b); }
 
 // ------------------------------------------------------------ mode traits
 template <int M>
@@ -399,7 +422,7 @@ struct Arith<TW> {
     static MWI T dxmul(double a, T b) { return dxtw_mul(a, b); }
     static MWI T dxadd(double a, T b) { return dxtw_add(a, b); }
     static MWI T norm(T a) { return a; }
-    static MWI T div(T a, T b) { return tw_div(a, b); }
+    static MWI T div(T a, T b) { return tw_div_t<true>(a, b); }
     static MWI double collapse(T a) { return __dadd_rn(__dadd_rn(a.w[0], a.w[1]), a.w[2]); }
 };
 template <>
@@ -414,6 +437,13 @@ struct Arith<QTW> {
     static MWI T div(T a, T b) { return tw_div(a, b); }
     static MWI double collapse(T a) { return __dadd_rn(__dadd_rn(a.w[0], a.w[1]), a.w[2]); }
 };
+
+// One out-of-line copy of a mode's addition, for code that runs once per
+// kernel (the last-CTA reduction of the tile partials): see "division" above.
+template <int M>
+__device__ __noinline__ V<Arith<M>::W> add_cold(V<Arith<M>::W> a, V<Arith<M>::W> b) {
+    return Arith<M>::add(a, b);
+}
 
 template <int W>
 MWI V<W> zero() {
