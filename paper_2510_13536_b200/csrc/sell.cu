@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <climits>
 #include <cstdlib>
+#include <cstring>
 #include <unordered_map>
 #include <vector>
 #include <cub/cub.cuh>
@@ -205,24 +206,40 @@ static int dia_patterns(SellMatrixOwned *M, const int64_t *val_ptr, const int64_
     std::vector<uint64_t> desc(2 * (size_t)(ns + DESC_PAD));
     std::unordered_multimap<uint64_t, std::pair<int64_t, int64_t>> seen;  // hash -> (pattern base, length)
     auto same = [](const ulonglong2 &a, const ulonglong2 &b) { return a.x == b.x && a.y == b.y; };
+    // consecutive slices of a stencil repeat a handful of patterns: the last
+    // few distinct ones are tried first (one memcmp each), the hash map only
+    // on a miss -- the loop is ~10 ns per slice instead of a hash + lookup
+    constexpr int RECENT = 4;
+    int64_t recent_base[RECENT], recent_len[RECENT];
+    int n_recent = 0, next_recent = 0;
     for (int64_t j = 0; j < ns; j++) {
         const int64_t b = rp[j], len = rp[j + 1] - rp[j];
-        uint64_t hsh = 1469598103934665603ull ^ (uint64_t)len;
-        for (int64_t k = 0; k < len; k++) {
-            hsh = (hsh ^ rc[b + k].x) * 1099511628211ull;
-            hsh = (hsh ^ rc[b + k].y) * 1099511628211ull;
-        }
         int64_t base = -1;
-        auto rng = seen.equal_range(hsh);
-        for (auto it = rng.first; it != rng.second && base < 0; ++it)
-            if (it->second.second == len &&
-                std::equal(rc.begin() + b, rc.begin() + b + len, pat.begin() + it->second.first, same))
-                base = it->second.first;
+        for (int r = 0; r < n_recent && base < 0; r++)
+            if (recent_len[r] == len &&
+                (len == 0 || std::memcmp(&rc[b], &pat[recent_base[r]], sizeof(ulonglong2) * (size_t)len) == 0))
+                base = recent_base[r];
         if (base < 0) {
-            base = (int64_t)pat.size();
-            pat.insert(pat.end(), rc.begin() + b, rc.begin() + b + len);
-            pat.insert(pat.end(), DIA_PAD, make_ulonglong2(0ull, 0ull));  // empty slots: chunks may read past the end
-            seen.emplace(hsh, std::make_pair(base, len));
+            uint64_t hsh = 1469598103934665603ull ^ (uint64_t)len;
+            for (int64_t k = 0; k < len; k++) {
+                hsh = (hsh ^ rc[b + k].x) * 1099511628211ull;
+                hsh = (hsh ^ rc[b + k].y) * 1099511628211ull;
+            }
+            auto rng = seen.equal_range(hsh);
+            for (auto it = rng.first; it != rng.second && base < 0; ++it)
+                if (it->second.second == len &&
+                    std::equal(rc.begin() + b, rc.begin() + b + len, pat.begin() + it->second.first, same))
+                    base = it->second.first;
+            if (base < 0) {
+                base = (int64_t)pat.size();
+                pat.insert(pat.end(), rc.begin() + b, rc.begin() + b + len);
+                pat.insert(pat.end(), DIA_PAD, make_ulonglong2(0ull, 0ull));  // empty slots: chunks may read past the end
+                seen.emplace(hsh, std::make_pair(base, len));
+            }
+            recent_base[next_recent] = base;
+            recent_len[next_recent] = len;
+            next_recent = (next_recent + 1) % RECENT;
+            n_recent = std::min(n_recent + 1, RECENT);
         }
         const uint64_t uni = (info[j] & DIA_UNIFORM_BIT) ? 1ull : 0ull;
         desc[2 * j] = (uint64_t)(vp[j] >> 5) | ((uint64_t)len << DIA_LBITS) | (uni << (DIA_LBITS + 8));
