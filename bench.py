@@ -62,6 +62,9 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--partitioned", action="store_true",
                     help="force the row-partitioned NCCL path (also at N=1 under torchrun)")
+    ap.add_argument("--pipeline", action="store_true",
+                    help="partitioned run: pipelined p exchange (one broadcast per rank slice, the "
+                         "column-block passes of a slice start when it has landed; dist.py)")
     ap.add_argument("--replicas", action="store_true",
                     help="N>1: independent replicas instead of the row-partitioned solver")
     ap.add_argument("--c5-rows", type=int, default=16_000_000,
@@ -621,7 +624,7 @@ def run_partitioned(a, world, rank, local, dist, torch):
                                                Aloc.values.clone())
     del Afull
     torch.cuda.empty_cache()
-    rs = RankSolver(Aloc, part, rank, mode)
+    rs = RankSolver(Aloc, part, rank, mode, pipeline=a.pipeline)
     del Aloc
     torch.cuda.empty_cache()
     setup_s = time.perf_counter() - t0

@@ -122,6 +122,15 @@ int mwcg_matrix_sigma_sorted(const mwcg_matrix *A); /* 1 if the rows of each til
  * row's running sum carried in q, so one pass gathers only a range of p that
  * fits the L2.  Same additions in the same order: bitwise-identical q. */
 int mwcg_matrix_col_blocks(const mwcg_matrix *A);   /* number of column blocks (0: not blocked) */
+int64_t mwcg_matrix_block_columns(const mwcg_matrix *A); /* columns per block (0: not blocked) */
+/* mwcg_matrix_create_ex with the caller's block width: cols_per_block > 0 cuts
+ * an int32-SELL matrix into ranges of that many columns, 0 builds none, < 0
+ * is the automatic choice.  The multi-GPU driver aligns the ranges with the
+ * ranks' slices of p (dist.py, pipelined exchange). */
+int mwcg_matrix_create_blocked(mwcg_matrix **out, int64_t n_rows, int64_t n_cols, int64_t nnz,
+                               const void *row_ptr, const void *col_idx, const double *values,
+                               int index_bytes, int64_t row_base, int col_format,
+                               int64_t cols_per_block, void *stream);
 int mwcg_matrix_destroy(mwcg_matrix *A);
 int mwcg_matrix_info(const mwcg_matrix *A, int64_t *n_rows, int64_t *n_cols, int64_t *nnz,
                      int64_t *padded_entries);
@@ -224,6 +233,13 @@ int mwcg_solver_create_dist(mwcg_solver **out, const mwcg_matrix *A, const mwcg_
 int mwcg_solver_set_interior(mwcg_solver *s, int64_t ilo, int64_t ihi);
 /* stream: NULL = the solver's stream (graph capture passes the capture stream) */
 int mwcg_solver_dist_stage(mwcg_solver *s, int stage, void *stream);
+/* SPMV restricted to the column blocks [b0, b1) of a blocked matrix (launch
+ * b starts from the running sums block b-1 left in q; the last block adds the
+ * p.q partials).  Calling it for [0, k1), [k1, k2) ... [kn, nblocks) in order is
+ * exactly SPMV -- and each call needs only the columns of its blocks, so the
+ * driver can run block b as soon as the rank owning those rows of p has
+ * delivered its slice (dist.py: pipelined exchange). */
+int mwcg_solver_dist_spmv_blocks(mwcg_solver *s, int b0, int b1, void *stream);
 
 /* ---- ingestion: Matrix Market coordinate text (sparse.py:115-196) ----
  * Two calls: with rows == NULL it parses the banner and size line into info;

@@ -68,6 +68,10 @@ SIGNATURES = {
     "mwcg_matrix_destroy": (ctypes.c_int, [c_vp]),
     "mwcg_matrix_stored_values": (c_i64, [c_vp]),
     "mwcg_matrix_col_blocks": (ctypes.c_int, [c_vp]),
+    "mwcg_matrix_block_columns": (c_i64, [c_vp]),
+    "mwcg_matrix_create_blocked": (ctypes.c_int, [ctypes.POINTER(c_vp), c_i64, c_i64, c_i64, c_vp, c_vp,
+                                                  c_vp, ctypes.c_int, c_i64, ctypes.c_int, c_i64, c_vp]),
+    "mwcg_solver_dist_spmv_blocks": (ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_int, c_vp]),
     "mwcg_matrix_info": (ctypes.c_int, [c_vp, ctypes.POINTER(c_i64), ctypes.POINTER(c_i64),
                                         ctypes.POINTER(c_i64), ctypes.POINTER(c_i64)]),
     "mwcg_spmv": (ctypes.c_int, [ctypes.c_int, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp]),

@@ -919,6 +919,7 @@ struct mwcg_solver {
     bool tma2 = false;                   // TMA-staged K2 (MWCG_TMA2=0/1 overrides)
     cudaAccessPolicyWindow l2win{};      // K1's persisting-L2 window over p (num_bytes 0: none)
     size_t l2_aside = 0;                 // the device's persisting set-aside (bytes)
+    int blk_lo = 0, blk_hi = -1;         // column blocks the next K1 launch walks ([lo, hi); hi < 0: all)
     int64_t ilo = 0, ihi = 0;            // interior tiles of a rank (SPMV_INTERIOR)
 };
 
@@ -958,12 +959,13 @@ void launch_k1(mwcg_solver *s, cudaStream_t st, cudaGraphConditionalHandle h, in
     const double *pc = s->p;
 #define K1_LAUNCH(CT) \
     cudaLaunchKernelEx(&cfg, cg_spmv_pq<M, FUSED, CT>, s->A, pc, s->q, g, s->part, s->st, h, use_cond)
-    const bool whole = g.a0 == 0 && g.a1 == g.ntiles && g.b0 == g.b1;  // not an interior/boundary split
-    if (!s->blocks.empty() && whole) {
+    if (!s->blocks.empty()) {  // (any tile subset: the running sums in q are per row)
         // column blocks: one launch per block, the row sums carried in q; each
         // launch pins ITS range of p in L2 (the block is sized to fit)
         const size_t nblk = s->blocks.size();
-        for (size_t b = 0; b < nblk; b++) {
+        const size_t b_lo = s->blk_hi < 0 ? 0 : (size_t)s->blk_lo;
+        const size_t b_hi = s->blk_hi < 0 ? nblk : std::min(nblk, (size_t)s->blk_hi);
+        for (size_t b = b_lo; b < b_hi; b++) {
             Geo gb = g;
             gb.acc_in = b > 0;
             gb.acc_out = b + 1 < nblk;
@@ -1298,6 +1300,13 @@ int mwcg_matrix_create(mwcg_matrix **out, int64_t n_rows, int64_t n_cols, int64_
 int mwcg_matrix_create_ex(mwcg_matrix **out, int64_t n_rows, int64_t n_cols, int64_t nnz, const void *row_ptr,
                           const void *col_idx, const double *values, int index_bytes, int64_t row_base,
                           int col_format, void *stream) {
+    return mwcg_matrix_create_blocked(out, n_rows, n_cols, nnz, row_ptr, col_idx, values, index_bytes, row_base,
+                                      col_format, -1, stream);
+}
+
+int mwcg_matrix_create_blocked(mwcg_matrix **out, int64_t n_rows, int64_t n_cols, int64_t nnz,
+                               const void *row_ptr, const void *col_idx, const double *values, int index_bytes,
+                               int64_t row_base, int col_format, int64_t cols_per_block, void *stream) {
     if (!out) {
         set_error("null output handle");
         return MWCG_ERR_VALUE;
@@ -1313,6 +1322,7 @@ int mwcg_matrix_create_ex(mwcg_matrix **out, int64_t n_rows, int64_t n_cols, int
     // the matrix has at least twice as many.
     int64_t cpb = (n_cols >= ((int64_t)1 << 22)) ? ((int64_t)1 << 21) : 0;
     if (const char *e = std::getenv("MWCG_COLBLOCK")) cpb = std::atoll(e);
+    if (cols_per_block >= 0) cpb = cols_per_block;  // the caller's choice (0: none)
     rc = sell_colblocks(A->blocks, M, row_ptr, col_idx, values, index_bytes, cpb, (cudaStream_t)stream);
     if (rc) {
         sell_destroy(M);
@@ -1324,6 +1334,10 @@ int mwcg_matrix_create_ex(mwcg_matrix **out, int64_t n_rows, int64_t n_cols, int
 }
 
 int mwcg_matrix_col_blocks(const mwcg_matrix *A) { return A ? (int)A->blocks.size() : -1; }
+
+int64_t mwcg_matrix_block_columns(const mwcg_matrix *A) {
+    return (A && !A->blocks.empty()) ? A->blocks[0]->col1 - A->blocks[0]->col0 : 0;
+}
 
 int mwcg_matrix_sigma_sorted(const mwcg_matrix *A) { return A && A->M->view.perm ? 1 : 0; }
 
@@ -1558,6 +1572,24 @@ int mwcg_solver_dist_stage(mwcg_solver *s, int stage, void *stream) {
     case TW: return enqueue_dist_stage<TW>(s, stage);
     default: return enqueue_dist_stage<QTW>(s, stage);
     }
+}
+
+int mwcg_solver_dist_spmv_blocks(mwcg_solver *s, int b0, int b1, void *stream) {
+    if (!s || !s->dist) {
+        set_error("not a distributed solver");
+        return MWCG_ERR_STATE;
+    }
+    if (s->blocks.empty() || b0 < 0 || b1 < b0 || b1 > (int)s->blocks.size()) {
+        set_error("bad column-block range [%d, %d) of %d", b0, b1, (int)s->blocks.size());
+        return MWCG_ERR_VALUE;
+    }
+    if (b0 == b1) return 0;
+    s->blk_lo = b0;
+    s->blk_hi = b1;
+    const int rc = mwcg_solver_dist_stage(s, MWCG_STAGE_SPMV, stream);
+    s->blk_lo = 0;
+    s->blk_hi = -1;
+    return rc;
 }
 
 int mwcg_solver_describe(const mwcg_solver *s, int64_t *out, int n) {

@@ -12,6 +12,16 @@ ntiles)), i.e. global rows [r*tmax*TILE, ...).  Each rank keeps
   * the tile partials of ALL ranks, rank-blocked, shape (R, w, tmax): every
     rank writes its own block and ONE all-gather completes the array.
 
+Pipelined exchange (opt-in, `pipeline=True`; irregular matrices whose p exchange
+is the all-gather: C5).  The rank's matrix is cut into column blocks (sell.cu)
+whose width divides the ranks' slice of p, so the blocks [s*m, (s+1)*m) hold
+exactly the columns owned by rank s.  A row's sum runs left to right through the
+blocks, i.e. through the ranks' slices in rank order -- so instead of one
+all-gather followed by the whole SpMV, rank s's slice is BROADCAST (R broadcasts,
+issued back to back on the communication stream) and the block passes of slice s
+start as soon as broadcast s has landed: the transfer of slice s+1.. overlaps the
+passes over slice s.  Same additions in the same order: bitwise identical.
+
 Per iteration:  [start the p exchange] -> SpMV of the interior tiles (rows
 that read only this rank's slice of p) -> [finish the exchange] -> SpMV of
 the boundary tiles (+p.q partials) -> gather partials -> finalize(alpha)
@@ -43,6 +53,7 @@ from .kernels import device_matrix, mode_words
 from .sparse import CsrMatrix
 
 TILE = 1024
+PIPELINE_BLOCK_COLUMNS = 1 << 21   # widest column block of the pipelined exchange (a 32-MB range of a DW p)
 
 __all__ = ["Partition", "partition", "local_rows", "RankSolver", "LocalExchange",
            "TorchDistExchange", "dist_cg_solve", "DistResult"]
@@ -152,7 +163,8 @@ def interior_tiles(A_local, lo, hi):
 class RankSolver:
     """Device state of one rank (any device; several may share a GPU)."""
 
-    def __init__(self, A_local, part, rank, mode, normalization="after-axpy", device=None):
+    def __init__(self, A_local, part, rank, mode, normalization="after-axpy", device=None,
+                 pipeline=False):
         dev = torch.device(device or "cuda")
         self.part, self.rank, self.mode = part, rank, mode
         self.w = w = mode_words(mode)
@@ -164,7 +176,18 @@ class RankSolver:
         # rank-blocked tile partials (include/mwcg_cuda.h): rank r's block of
         # w * tmax doubles at r * w * tmax
         self.partials = torch.zeros(part.world * w * part.tmax, dtype=torch.float64, device=dev)
-        self.dm = device_matrix(A_local, row_base=self.lo)
+        # pipelined exchange: column blocks aligned with the ranks' slices of p
+        # (m blocks per slice, each at most 2^21 columns wide)
+        self.blocks_per_slice = 0
+        if pipeline:
+            m = 1
+            while part.nmax // m > PIPELINE_BLOCK_COLUMNS or part.nmax % m:
+                m += 1
+            self.dm = device_matrix(A_local, row_base=self.lo, col_block=part.nmax // m)
+            if self.dm.col_blocks() > 0 and self.dm.block_columns() * m == part.nmax:
+                self.blocks_per_slice = m
+        else:
+            self.dm = device_matrix(A_local, row_base=self.lo)
         L = _lib.load()
         self._L = L
         cfg = _lib.SolverConfigC(_lib.MODE_ID[mode], _lib.NORM_ID[normalization], 0, 0, 1)
@@ -209,6 +232,17 @@ class RankSolver:
     def stage(self, name):
         _lib.check(self._L.mwcg_solver_dist_stage(self.handle, _lib.STAGE[name],
                                                   _lib.stream_handle()))
+
+    def spmv_slice(self, src):
+        """The block passes over the columns owned by rank `src` (pipelined
+        exchange); after src = world - 1 the SpMV and its p.q partials are complete."""
+        m = self.blocks_per_slice
+        nb = self.dm.col_blocks()
+        b0, b1 = min(src * m, nb), min((src + 1) * m, nb)
+        if src == self.part.world - 1:
+            b1 = nb
+        if self.n > 0 and b1 > b0:
+            _lib.check(self._L.mwcg_solver_dist_spmv_blocks(self.handle, b0, b1, _lib.stream_handle()))
 
     def state(self):
         s = _lib.StateC()
@@ -269,6 +303,19 @@ class LocalExchange:
 
     def finish(self, handle):
         self.gather(*handle)
+
+    # pipelined exchange: nothing moves at start; slice s is copied when it is
+    # waited for, so a block pass issued before its slice would read stale p
+    def start_slices(self, ranks):
+        return ranks
+
+    def finish_slice(self, ranks, src):
+        for s_rank in ranks:
+            if s_rank.rank == src:
+                for j, (buf, off, cnt) in enumerate(s_rank.segments("p")):
+                    for dst in ranks:
+                        if dst is not s_rank:
+                            dst.segments("p")[j][0][off:off + cnt].copy_(buf[off:off + cnt])
 
     def gather(self, ranks, which):
         if which == "p" and self.pieces is not None:
@@ -347,6 +394,23 @@ class TorchDistExchange:
             for o, t in zip(outs, tmp):
                 o.copy_(t)
 
+    # pipelined exchange: one broadcast per source rank, all issued up front in
+    # rank order (the same order on every rank); finish_slice(src) makes the
+    # current stream wait for slice src only
+    def start_slices(self, ranks):
+        (me,) = ranks
+        world = self.dist.get_world_size(self.group)
+        return [[self.dist.broadcast(buf[s * cnt:(s + 1) * cnt], src=self._global(s), group=self.group,
+                                     async_op=True) for buf, _, cnt in me.segments("p")]
+                for s in range(world)]
+
+    def _global(self, group_rank):
+        return self.dist.get_global_rank(self.group, group_rank) if self.group is not None else group_rank
+
+    def finish_slice(self, works, src):
+        for w in works[src]:
+            w.wait()
+
     def gather(self, ranks, which):
         self.finish(self.start(ranks, which))
 
@@ -366,16 +430,32 @@ def _kernels_per_iteration(rs):
     finalize(beta), XPAY."""
     ilo, ihi = getattr(rs, "interior", (0, 0))
     nt = (rs.n + TILE - 1) // TILE
-    return 4 + (1 if ihi > ilo else 0) + (1 if nt - (ihi - ilo) > 0 else 0)
+    dm = getattr(rs, "dm", None)
+    per_spmv = max(1, dm.col_blocks()) if dm is not None else 1   # one launch per column block
+    if getattr(rs, "blocks_per_slice", 0) > 0:
+        return 4 + per_spmv                                     # pipelined: every block once
+    return 4 + per_spmv * ((1 if ihi > ilo else 0) + (1 if nt - (ihi - ilo) > 0 else 0))
+
+
+def _pipelined(ranks, exchange):
+    return (getattr(exchange, "mode", None) == "allgather" and hasattr(exchange, "start_slices")
+            and all(getattr(rs, "blocks_per_slice", 0) > 0 for rs in ranks))
 
 
 def _iteration(ranks, exchange):
-    h = exchange.start(ranks, "p")       # p slices written by the last XPAY / init
-    for rs in ranks:
-        rs.stage("spmv_interior")        # overlaps the exchange
-    exchange.finish(h)
-    for rs in ranks:
-        rs.stage("spmv_boundary")
+    if _pipelined(ranks, exchange):
+        h = exchange.start_slices(ranks)     # R broadcasts, back to back
+        for src in range(ranks[0].part.world):
+            exchange.finish_slice(h, src)    # slice src has landed
+            for rs in ranks:
+                rs.spmv_slice(src)           # ... its block passes overlap the later broadcasts
+    else:
+        h = exchange.start(ranks, "p")       # p slices written by the last XPAY / init
+        for rs in ranks:
+            rs.stage("spmv_interior")        # overlaps the exchange
+        exchange.finish(h)
+        for rs in ranks:
+            rs.stage("spmv_boundary")
     exchange.gather(ranks, "part")
     for rs in ranks:
         rs.stage("final_alpha")
@@ -451,7 +531,7 @@ def dist_cg_solve(ranks, exchange, b_norm, epsilon=1e-12, max_iterations=None,
 
 def solve_partitioned(A, b, world, mode="dw", epsilon=1e-12, max_iterations=None, x0=None,
                       normalization="after-axpy", exchange=None, ranks_here=None,
-                      check_every=16, graph=False):
+                      check_every=16, graph=False, pipeline=False):
     """Convenience: build the rank solvers for `ranks_here` (default: all
     ranks, emulated in this process) and solve.  Returns (result, x words of
     the local ranks concatenated)."""
@@ -468,7 +548,7 @@ def solve_partitioned(A, b, world, mode="dw", epsilon=1e-12, max_iterations=None
     ranks = []
     for r in ranks_here:
         lo, hi = part.rows(r)
-        rs = RankSolver(local_rows(A, lo, hi), part, r, mode, normalization)
+        rs = RankSolver(local_rows(A, lo, hi), part, r, mode, normalization, pipeline=pipeline)
         b_loc = torch.from_numpy(np.ascontiguousarray(b[lo:hi])).cuda() if hi > lo else \
             torch.zeros(1, dtype=torch.float64, device="cuda")
         rs.start(b_loc, _b_norm(b), x0_full, epsilon, max_iterations if max_iterations is not None

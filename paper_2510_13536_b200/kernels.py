@@ -113,12 +113,14 @@ class MultiwordVector:
 
 
 # ---------------------------------------------------------------- matrices
-def device_matrix(A, row_base=0, col_format=-1):
+def device_matrix(A, row_base=0, col_format=-1, col_block=-1):
     """SELL-32 device copy of a CsrMatrix, built once and cached on A.
     row_base: global index of row 0 when A holds a rank's rows with global
     columns (dist.py); col_format: -1 auto / 0 int32 / 1 int16 deltas /
     2 slice-shared offsets, optionally | _lib.SELL_SIGMA / _lib.SELL_NO_SIGMA /
-    _lib.DIA_STREAM_VALUES ("auto" is 15 with a flag) (include/mwcg_cuda.h)."""
+    _lib.DIA_STREAM_VALUES ("auto" is 15 with a flag) (include/mwcg_cuda.h).
+    col_block: columns per column block of an irregular (int32-SELL) matrix
+    (-1 automatic, 0 none)."""
     h = getattr(A, "_device", None)
     if h is not None:
         return h
@@ -138,9 +140,9 @@ def device_matrix(A, row_base=0, col_format=-1):
             va = torch.from_numpy(np.ascontiguousarray(A.values, dtype=np.float64)).to(dev, non_blocking=True)
         ib = 8
     handle = ctypes.c_void_p()
-    _lib.check(L.mwcg_matrix_create_ex(ctypes.byref(handle), A.n_rows, A.n_cols, A.nnz,
-                                       _lib.ptr(rp), _lib.ptr(ci), _lib.ptr(va), ib, int(row_base),
-                                       int(col_format), _lib.stream_handle()))
+    _lib.check(L.mwcg_matrix_create_blocked(ctypes.byref(handle), A.n_rows, A.n_cols, A.nnz,
+                                            _lib.ptr(rp), _lib.ptr(ci), _lib.ptr(va), ib, int(row_base),
+                                            int(col_format), int(col_block), _lib.stream_handle()))
     dm = _DeviceMatrix(handle, A.n_rows, A.n_cols, A.nnz)
     try:
         object.__setattr__(A, "_device", dm)
@@ -170,6 +172,10 @@ class _DeviceMatrix:
     def col_blocks(self):
         """Number of column blocks K1 walks (0: the matrix is not blocked)."""
         return int(_lib.load().mwcg_matrix_col_blocks(self.handle))
+
+    def block_columns(self):
+        """Columns per column block (0: not blocked)."""
+        return int(_lib.load().mwcg_matrix_block_columns(self.handle))
 
     def stored_values(self):
         """Value entries the layout stores and streams per SpMV (value-uniform

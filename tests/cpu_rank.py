@@ -16,8 +16,13 @@ from oracle import oracle as orc
 
 
 class CpuRank:
-    def __init__(self, A_local, part, rank, mode, normalization="after-axpy"):
+    def __init__(self, A_local, part, rank, mode, normalization="after-axpy", pipeline=False):
         self.part, self.rank, self.mode = part, rank, mode
+        # pipelined exchange (dist.py): one "block" per rank slice; spmv_slice(s)
+        # records slice s of p AS IT IS when its pass runs, and the SpMV after the
+        # last slice uses that record -- a pass issued before its slice arrived
+        # would freeze stale data and break the bitwise comparison
+        self.blocks_per_slice = 1 if pipeline else 0
         self.w = w = orc.WORDS[mode]
         self.lo, self.hi = part.rows(rank)
         self.n = self.hi - self.lo
@@ -158,6 +163,20 @@ class CpuRank:
                 if self.norm_all:
                     pl = orc.normalize(m, pl)
                 self.p_full.numpy()[:, self.lo:self.hi] = pl
+
+    def spmv_slice(self, src):
+        if self.st.status != 0:
+            return
+        if src == 0:
+            self._seen = np.zeros_like(self.p_full.numpy())
+        lo = src * self.part.nmax
+        self._seen[:, lo:lo + self.part.nmax] = self.p_full.numpy()[:, lo:lo + self.part.nmax]
+        if src == self.part.world - 1 and self.n:
+            q = orc.spmv(self.mode, self.A, self._seen)
+            if self.norm_all:
+                q = orc.normalize(self.mode, q)
+            self.q = q
+            self._partials_of(self._pl(), self.q)
 
     def state(self):
         s = self.st

@@ -33,7 +33,7 @@ def _matrix(kind, k):
     return laplacian_2d(k) if kind == "lap" else random_symmetric(k * k, seed=3)
 
 
-def _worker(rank, world, port, mode, k, outdir, kind):
+def _worker(rank, world, port, mode, k, outdir, kind, pipeline=False):
     import sys
     if ROOT not in sys.path:
         sys.path.insert(0, ROOT)
@@ -56,7 +56,7 @@ def _worker(rank, world, port, mode, k, outdir, kind):
         b = problems.spmv_fp64_host(A, xs)
         part = partition(A.n_rows, world)
         lo, hi = part.rows(rank)
-        rs = CpuRank(local_rows(A, lo, hi), part, rank, mode)
+        rs = CpuRank(local_rows(A, lo, hi), part, rank, mode, pipeline=pipeline)
         s = 0.0
         for v in b:
             s = s + v * v
@@ -65,8 +65,9 @@ def _worker(rank, world, port, mode, k, outdir, kind):
         res = dist_cg_solve([rs], ex, float(np.sqrt(s)),
                             1e-20 if mode != "fp64" else 1e-12, 2000, check_every=4)
         np.save(os.path.join(outdir, f"x{rank}.npy"), rs.x)
+        from paper_2510_13536_b200.dist import _pipelined
         with open(os.path.join(outdir, f"mode{rank}.txt"), "w") as f:
-            f.write(ex.mode)
+            f.write(ex.mode + ("+pipelined" if _pipelined([rs], ex) else ""))
         np.save(os.path.join(outdir, f"it{rank}.npy"),
                 np.array([res.iterations, res.final_recurrence_residual]))
     finally:
@@ -96,6 +97,31 @@ def test_partitioned_solve_gloo_matches_single(world, mode, kind, tmp_path):
     assert np.array_equal(x.view(np.uint64), ref.x.view(np.uint64))
     # banded matrix: neighbour halo; random columns: all-gather of p
     want = "halo" if kind == "lap" else "allgather"
+    assert all((tmp_path / f"mode{r}.txt").read_text() == want for r in range(world))
+
+
+@pytest.mark.parametrize("world,mode", [(2, "dw"), (3, "qtw")])
+def test_pipelined_slice_broadcasts_gloo(world, mode, tmp_path):
+    """The pipelined exchange of dist.py (one broadcast per rank slice, the
+    passes over slice s issued once broadcast s has completed) over gloo:
+    bitwise the single-process solve."""
+    k = 60 if world == 2 else 100   # world 3 at n = 3600 would leave a rank without rows and use halos
+    port = _free_port()
+    mp.start_processes(_worker, args=(world, port, mode, k, str(tmp_path), "rand", True), nprocs=world,
+                       join=True, start_method="spawn")
+    from oracle import oracle as orc
+    from paper_2510_13536_b200 import problems
+    A = _matrix("rand", k)
+    xs = np.random.default_rng(4).uniform(-1, 1, A.n_rows)
+    b = problems.spmv_fp64_host(A, xs)
+    ref = orc.cg_solve(A, b, mode=mode, epsilon=1e-20, max_iterations=2000, reduction="tile",
+                       record_history=False)
+    x = np.concatenate([np.load(tmp_path / f"x{r}.npy") for r in range(world)], axis=1)
+    its = [np.load(tmp_path / f"it{r}.npy") for r in range(world)]
+    assert all(int(i[0]) == ref.iterations for i in its)
+    assert np.array_equal(x.view(np.uint64), ref.x.view(np.uint64))
+    # random columns -> all-gather, replaced by the slice broadcasts
+    want = "allgather+pipelined"
     assert all((tmp_path / f"mode{r}.txt").read_text() == want for r in range(world))
 
 

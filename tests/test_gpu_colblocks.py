@@ -121,3 +121,42 @@ def test_blocked_partitioned_equals_single(world, monkeypatch):
     monkeypatch.delenv("MWCG_COLBLOCK")
     assert res.iterations == single.iterations
     assert np.array_equal(x.cpu().numpy().view(np.uint64), single.x.planes.cpu().numpy().view(np.uint64))
+
+
+@pytest.mark.parametrize("world", [2, 3, 5])
+@pytest.mark.parametrize("mode", ["dw", "qtw"])
+def test_pipelined_slice_exchange_equals_single(world, mode):
+    """dist.py's pipelined exchange: the rank matrices are cut into column
+    blocks aligned with the ranks' slices of p and block passes of slice s run
+    when slice s has been delivered (LocalExchange copies it only then, so a
+    pass issued early would read stale p).  Bitwise the single-GPU solve."""
+    from paper_2510_13536_b200.dist import LocalExchange, RankSolver, _pipelined, partition
+    A = _c5(N)
+    b = np.random.default_rng(4).uniform(-1, 1, A.n_rows)
+    single = cg.cg_solve(_copy(A), b, cg.SolverConfig(mode=mode, epsilon=1e-24, history_stride=10**6))
+    res, x = solve_partitioned(_copy(A), b, world, mode=mode, epsilon=1e-24, max_iterations=2000,
+                               pipeline=True)
+    assert res.iterations == single.iterations and res.reason == single.reason
+    assert np.array_equal(x.cpu().numpy().view(np.uint64), single.x.planes.cpu().numpy().view(np.uint64))
+    # the pipelined path really ran: blocks aligned with the slices
+    part = partition(A.n_rows, world)
+    from paper_2510_13536_b200.dist import local_rows
+    lo, hi = part.rows(0)
+    rs = RankSolver(local_rows(_copy(A), lo, hi), part, 0, mode, pipeline=True)
+    assert rs.blocks_per_slice >= 1 and rs.dm.block_columns() * rs.blocks_per_slice == part.nmax
+    ex = LocalExchange()
+    ex.mode = "allgather"
+    assert _pipelined([rs], ex)
+
+
+def test_pipelined_exchange_with_several_blocks_per_slice(monkeypatch):
+    """Slices wider than a block: m > 1 blocks per slice (forced through a small
+    block limit)."""
+    import paper_2510_13536_b200.dist as D
+    A = _c5(N)
+    b = np.random.default_rng(4).uniform(-1, 1, A.n_rows)
+    single = cg.cg_solve(_copy(A), b, cg.SolverConfig(mode="dw", epsilon=1e-24, history_stride=10**6))
+    monkeypatch.setattr(D, "PIPELINE_BLOCK_COLUMNS", 10000)
+    res, x = solve_partitioned(_copy(A), b, 2, mode="dw", epsilon=1e-24, max_iterations=2000, pipeline=True)
+    assert res.iterations == single.iterations
+    assert np.array_equal(x.cpu().numpy().view(np.uint64), single.x.planes.cpu().numpy().view(np.uint64))

@@ -67,3 +67,34 @@ def test_nccl_world1_c2_slice(nccl_world1):
                                exchange=TorchDistExchange(), ranks_here=[0], graph=True)
     assert res.iterations == single.iterations
     assert np.array_equal(_bits(x), _bits(single.x.planes))
+
+
+@pytest.mark.parametrize("graph", [False, True])
+def test_nccl_world1_pipelined_slice_exchange(nccl_world1, graph):
+    """The pipelined exchange (dist.py: NCCL broadcast per rank slice + the
+    column-block passes of that slice) through NCCL at world 1, eager and
+    graph-captured: an irregular matrix wide enough for int32 columns."""
+    from paper_2510_13536_b200.dist import RankSolver, _pipelined, dist_cg_solve, local_rows, partition
+    from paper_2510_13536_b200.sparse import CsrMatrix
+    from paper_2510_13536_b200.cg import _b_norm
+    import paper_2510_13536_b200.dist as D
+    n = 72000 + 77
+    rp, col, val = problems.random_irregular_spd(n, seed=3, device="cpu")
+    A = CsrMatrix(n, n, rp.numpy().astype(np.int64), col.numpy().astype(np.int64), val.numpy())
+    b = np.random.default_rng(4).uniform(-1, 1, n)
+    single = cg.cg_solve(A, b, cg.SolverConfig(mode="dw", epsilon=1e-24, history_stride=10**6))
+    old = D.PIPELINE_BLOCK_COLUMNS
+    D.PIPELINE_BLOCK_COLUMNS = 20000   # several blocks inside the one slice
+    try:
+        part = partition(n, 1)
+        rs = RankSolver(local_rows(A, 0, n), part, 0, "dw", pipeline=True)
+    finally:
+        D.PIPELINE_BLOCK_COLUMNS = old
+    assert rs.blocks_per_slice >= 2
+    ex = TorchDistExchange()
+    bn = _b_norm(b)
+    rs.start(torch.from_numpy(b).cuda(), bn, None, 1e-24, 2000)
+    res = dist_cg_solve([rs], ex, bn, 1e-24, 2000, check_every=8, graph=graph)
+    assert _pipelined([rs], ex)
+    assert res.iterations == single.iterations and res.reason == single.reason
+    assert np.array_equal(_bits(rs.solution()), _bits(single.x.planes))
