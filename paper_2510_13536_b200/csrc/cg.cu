@@ -209,6 +209,13 @@ struct SpTraits {
 #else
     static constexpr int U = (M == FP64) ? 8 : ((M == TW) ? 3 : 4);  // measured per mode (C2)
 #endif
+    // rows of a thread walked in pairs when they share a uniform pattern
+    // (ops.cuh: spmv_pair_dia); UP: slots per chunk of a pair (<= 4), 0: off
+#ifdef MWCG_SP_PAIR_OVERRIDE
+    static constexpr int UP = MWCG_SP_PAIR_OVERRIDE;
+#else
+    static constexpr int UP = 0;
+#endif
     // chunk of a value-uniform slice (no value registers: ops.cuh)
 #ifdef MWCG_SP_UU_OVERRIDE
     static constexpr int UU = MWCG_SP_UU_OVERRIDE;
@@ -251,6 +258,34 @@ __global__ void __launch_bounds__(SpTraits<M>::THREADS, SpTraits<M>::MINB)
         int pos = tile * TILE + (int)threadIdx.x;
         SliceWords sw = slice_words<CT>(A, pos);
         V<W> acc = zero<W>();
+        constexpr int UP = SpTraits<M>::UP;
+        if constexpr (UP > 0 && std::is_same<CT, DiaTag>::value && !STAGE && FUSED && (TILE / NT) % 2 == 0) {
+            // pairs (pos, pos + NT): canonical p.q order kept (A's term, then B's)
+#pragma unroll 1
+            for (int k = 0; k < TILE / NT; k += 2, pos += 2 * NT) {
+                const int pb = pos + NT;
+                const SliceWords swa = k ? slice_words<CT>(A, pos) : sw;
+                const SliceWords swb = slice_words<CT>(A, pb);
+                V<W> sa = zero<W>(), sb = zero<W>();
+                bool done = false;
+                if (pb < n) done = spmv_pair_dia<M, UP, true>(A, p, 0, pos, pb, swa, swb, sa, sb);
+                if (!done) {
+                    if (pos < n) sa = spmv_row<M, SpTraits<M>::U, CT, true, SpTraits<M>::UU>(A, p, 0, pos, swa);
+                    if (pb < n) sb = spmv_row<M, SpTraits<M>::U, CT, true, SpTraits<M>::UU>(A, p, 0, pb, swb);
+                }
+                if (pos < n) {
+                    if (norm_all) sa = Ar::norm(sa);
+                    acc = Ar::add(acc, Ar::mul(load_aos_ro<W>(pl + (int64_t)pos * W, 0), sa));
+                    store<W>(q + pos, g.ld, 0, sa);
+                }
+                if (pb < n) {
+                    if (norm_all) sb = Ar::norm(sb);
+                    acc = Ar::add(acc, Ar::mul(load_aos_ro<W>(pl + (int64_t)pb * W, 0), sb));
+                    store<W>(q + pb, g.ld, 0, sb);
+                }
+            }
+            pos -= NT;  // the tile is read back from pos below
+        } else
 #pragma unroll 1
         for (;;) {
             const bool more = ((pos + NT) >> 10) == (pos >> 10);

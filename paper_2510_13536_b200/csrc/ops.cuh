@@ -205,6 +205,66 @@ __device__ __forceinline__ void dia_walk(mw::V<mw::Arith<M>::W> &s, int L, const
     }
 }
 
+// Two rows of one thread walked TOGETHER (rows pos and pos + NT of a tile) when
+// both sit in value-uniform slices with the SAME pattern (interior stencil
+// rows): the slot records are loaded once, each slot's two gathers issue
+// together and the two multi-word sums advance as independent dependency
+// chains.  A dependent FP64 operation issues every ~20 cycles, so one chain per
+// warp with 8 warps per scheduler leaves the FP64 pipe at ~45 %; two chains per
+// thread double the arithmetic in flight without more warps.  Each row's own
+// additions and their order are unchanged.
+template <int M, int N, bool XAOS>
+__device__ __forceinline__ void dia_chunk_pair(mw::V<mw::Arith<M>::W> &sa, mw::V<mw::Arith<M>::W> &sb,
+                                               const ulonglong2 *__restrict__ op,
+                                               const double *__restrict__ xga, const double *__restrict__ xgb,
+                                               int64_t ldx, uint32_t lbit) {
+    using Ar = mw::Arith<M>;
+    constexpr int W = Ar::W;
+    double a[N];
+    bool ok[N];
+    mw::V<W> xa[N], xb[N];
+#pragma unroll
+    for (int u = 0; u < N; u++) {
+        const ulonglong2 rec = __ldg(op + u);
+        a[u] = __longlong_as_double((long long)rec.y);
+        ok[u] = ((uint32_t)(rec.x >> 32) & lbit) != 0;
+        const int off = ok[u] ? (int)(uint32_t)rec.x : 0;
+        xa[u] = dia_gather<W, XAOS>(xga, ldx, off);
+        xb[u] = dia_gather<W, XAOS>(xgb, ldx, off);
+    }
+#pragma unroll
+    for (int u = 0; u < N; u++) {
+        sa = keep_if<W>(ok[u], Ar::add(sa, Ar::dxmul(a[u], xa[u])), sa);
+        sb = keep_if<W>(ok[u], Ar::add(sb, Ar::dxmul(a[u], xb[u])), sb);
+    }
+}
+
+// true (and both sums computed) when the pair could be walked together;
+// false: the caller walks the rows one by one
+template <int M, int UP, bool XAOS>
+__device__ __forceinline__ bool spmv_pair_dia(const SellMatrix &A, const double *__restrict__ x, int64_t ldx,
+                                              int64_t rowa, int64_t rowb, SliceWords swa, SliceWords swb,
+                                              mw::V<mw::Arith<M>::W> &sa, mw::V<mw::Arith<M>::W> &sb) {
+    constexpr int W = mw::Arith<M>::W;
+    const uint32_t fa = (uint32_t)((uint64_t)swa.w0 >> DIA_LBITS), fb = (uint32_t)((uint64_t)swb.w0 >> DIA_LBITS);
+    // same pattern base, both uniform (then the slot counts agree too)
+    if (swa.w1 != swb.w1 || ((fa & fb) & 0x100u) == 0 || ((fa ^ fb) & 0xffu) != 0) return false;
+    const int L = (int)(fa & 0xffu);
+    const uint32_t lbit = 1u << ((int)rowa & 31);
+    const double *__restrict__ xga = x + (A.row_base + rowa) * (XAOS ? W : 1);
+    const double *__restrict__ xgb = x + (A.row_base + rowb) * (XAOS ? W : 1);
+    const ulonglong2 *__restrict__ op = A.pat + swa.w1;
+    sa = mw::zero<W>();
+    sb = mw::zero<W>();
+    int k0 = 0;
+    for (; k0 + UP <= L; k0 += UP, op += UP) dia_chunk_pair<M, UP, XAOS>(sa, sb, op, xga, xgb, ldx, lbit);
+    const int rem = L - k0;
+    if (UP > 1 && rem == 1) dia_chunk_pair<M, 1, XAOS>(sa, sb, op, xga, xgb, ldx, lbit);
+    if (UP > 2 && rem == 2) dia_chunk_pair<M, 2, XAOS>(sa, sb, op, xga, xgb, ldx, lbit);
+    if (UP > 3 && rem == 3) dia_chunk_pair<M, 3, XAOS>(sa, sb, op, xga, xgb, ldx, lbit);
+    return true;
+}
+
 template <int M, int U, bool XAOS, int UU = U>
 __device__ __forceinline__ mw::V<mw::Arith<M>::W> spmv_row_dia(const SellMatrix &A,
                                                                const double *__restrict__ x, int64_t ldx,
