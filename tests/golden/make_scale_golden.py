@@ -39,13 +39,14 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", default="")
     ap.add_argument("--threads", type=int, default=os.cpu_count())
+    ap.add_argument("--out", default=OUT, help="result file (merge several partial files by hand)")
     a = ap.parse_args()
     plan = PLAN
     if a.only:
         want = {tuple(s.split(":")) for s in a.only.split(",")}
         plan = [p for p in PLAN if p in want]
     orc.set_threads(a.threads)
-    out = json.load(open(OUT)) if os.path.exists(OUT) else {}
+    out = json.load(open(a.out)) if os.path.exists(a.out) else {}
     cache = {}
     for name, mode in plan:
         if mode in out.get(name, {}).get("runs", {}):
@@ -71,7 +72,7 @@ def main():
                              "error_norm": err, "partitions": 1, "seconds": round(dt, 1),
                              "threads": a.threads}
         print(name, mode, json.dumps(ent["runs"][mode]), flush=True)
-        json.dump(out, open(OUT, "w"), indent=1, sort_keys=True)
+        json.dump(out, open(a.out, "w"), indent=1, sort_keys=True)
 
 
 if __name__ == "__main__":
