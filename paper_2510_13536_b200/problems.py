@@ -287,5 +287,15 @@ def config5_style(n=1_000_000, seed=3):
     return dict(name="C5s", A=A, b=b, x_star=None, epsilon=1e-12, max_iterations=20000)
 
 
+def config4_style(n=100_000):
+    """A C4-style instance (the config-4 generator at n = 1e5: same band, same
+    10^U(0,6) diagonal scaling, so precision still moves the iteration count)
+    small enough for host solves of the reference order in every arithmetic
+    (parity at scale, tests/golden/scale.json)."""
+    c = config4(n=n)
+    c["name"] = "C4s"
+    return c
+
+
 CONFIGS = {"C1": config1, "C2": config2, "C3": config3, "C4": config4, "C5": config5,
-           "C5s": config5_style}
+           "C5s": config5_style, "C4s": config4_style}

@@ -32,6 +32,7 @@ OUT = os.path.join(HERE, "scale.json")
 PLAN = [("C2", m) for m in ("fp64", "dw", "qdw", "qtw", "tw")] + \
        [("C3", m) for m in ("fp64", "dw", "qdw", "qtw")] + \
        [("C5s", m) for m in ("dw", "qtw")] + \
+       [("C4s", m) for m in ("fp64", "dw", "qdw", "qtw", "tw")] + \
        [("C4", m) for m in ("dw", "qtw", "fp64", "qdw")] + [("C3", "tw"), ("C4", "tw")]
 
 

@@ -38,7 +38,7 @@ def _problem(name):
 
 def _cases():
     out = []
-    for name in ("C2", "C3", "C5s", "C4"):
+    for name in ("C2", "C3", "C5s", "C4s", "C4"):
         for mode in ("fp64", "dw", "qdw", "tw", "qtw"):
             if mode in GOLD.get(name, {}).get("runs", {}):
                 out.append((name, mode))
