@@ -145,7 +145,9 @@ __device__ __forceinline__ mw::V<W> keep_if(bool ok, mw::V<W> t, mw::V<W> s) {
 // a slot gathers its own row (always in bounds), multiplies, and keeps its
 // old sum by a select.  (With a branch on the lane predicate the compiler
 // sinks each slot's loads into its branch: one memory round trip per entry.)
-template <int M, int N, bool XAOS, bool UNIFORM>
+// FULL: every slot of the slice is present in all 32 rows (interior stencil /
+// band slices): no lane predicate, no offset select, no keep-select.
+template <int M, int N, bool XAOS, bool UNIFORM, bool FULL = false>
 __device__ __forceinline__ void dia_chunk(mw::V<mw::Arith<M>::W> &s, const ulonglong2 *__restrict__ op,
                                           const double *__restrict__ vp, const double *__restrict__ xg,
                                           int64_t ldx, uint32_t lbit, const SellMatrix &A, int64_t grow) {
@@ -167,16 +169,19 @@ __device__ __forceinline__ void dia_chunk(mw::V<mw::Arith<M>::W> &s, const ulong
             om = __ldg(&op[u].x);
             a[u] = ld_stream(vp + u * SLICE);
         }
-        ok[u] = ((uint32_t)(om >> 32) & lbit) != 0;
+        ok[u] = FULL || ((uint32_t)(om >> 32) & lbit) != 0;
+        MWCG_ASSERT(!FULL || (uint32_t)(om >> 32) == 0xffffffffu);
         MWCG_ASSERT(!ok[u] || (grow + (int)(uint32_t)om >= 0 && grow + (int)(uint32_t)om < A.n_cols));
         xv[u] = dia_gather<W, XAOS>(xg, ldx, ok[u] ? (int)(uint32_t)om : 0);
     }
     // streamed TW/QTW rows keep the lane branch (C4 QTW K1: 78 us against
     // 87 us branch-free; every other case is as fast or faster branch-free)
-    constexpr bool BRANCHY = !UNIFORM && W == 3;
+    constexpr bool BRANCHY = !UNIFORM && W == 3 && !FULL;
 #pragma unroll
     for (int u = 0; u < N; u++) {
-        if (BRANCHY) {
+        if (FULL) {
+            s = Ar::add(s, Ar::dxmul(a[u], xv[u]));
+        } else if (BRANCHY) {
             if (ok[u]) s = Ar::add(s, Ar::dxmul(a[u], xv[u]));
         } else {
             s = keep_if<W>(ok[u], Ar::add(s, Ar::dxmul(a[u], xv[u])), s);
@@ -185,23 +190,23 @@ __device__ __forceinline__ void dia_chunk(mw::V<mw::Arith<M>::W> &s, const ulong
 }
 
 // the slots of a row: full chunks of U, then one exact chunk for the rest
-template <int M, int U, bool XAOS, bool UNIFORM>
+template <int M, int U, bool XAOS, bool UNIFORM, bool FULL = false>
 __device__ __forceinline__ void dia_walk(mw::V<mw::Arith<M>::W> &s, int L, const ulonglong2 *__restrict__ op,
                                          const double *__restrict__ vp, const double *__restrict__ xg,
                                          int64_t ldx, uint32_t lbit, const SellMatrix &A, int64_t grow) {
     int k0 = 0;
-    for (; k0 + U <= L; k0 += U, op += U, vp += U * SLICE) dia_chunk<M, U, XAOS, UNIFORM>(s, op, vp, xg, ldx, lbit, A, grow);
+    for (; k0 + U <= L; k0 += U, op += U, vp += U * SLICE) dia_chunk<M, U, XAOS, UNIFORM, FULL>(s, op, vp, xg, ldx, lbit, A, grow);
     const int rem = L - k0;
-    if (U > 1 && rem == 1) dia_chunk<M, 1, XAOS, UNIFORM>(s, op, vp, xg, ldx, lbit, A, grow);
-    if (U > 2 && rem == 2) dia_chunk<M, 2, XAOS, UNIFORM>(s, op, vp, xg, ldx, lbit, A, grow);
-    if (U > 3 && rem == 3) dia_chunk<M, 3, XAOS, UNIFORM>(s, op, vp, xg, ldx, lbit, A, grow);
+    if (U > 1 && rem == 1) dia_chunk<M, 1, XAOS, UNIFORM, FULL>(s, op, vp, xg, ldx, lbit, A, grow);
+    if (U > 2 && rem == 2) dia_chunk<M, 2, XAOS, UNIFORM, FULL>(s, op, vp, xg, ldx, lbit, A, grow);
+    if (U > 3 && rem == 3) dia_chunk<M, 3, XAOS, UNIFORM, FULL>(s, op, vp, xg, ldx, lbit, A, grow);
     if (U > 4 && rem >= 4) {  // U up to 8: 4 + (rem - 4)
-        dia_chunk<M, 4, XAOS, UNIFORM>(s, op, vp, xg, ldx, lbit, A, grow);
+        dia_chunk<M, 4, XAOS, UNIFORM, FULL>(s, op, vp, xg, ldx, lbit, A, grow);
         op += 4;
         vp += 4 * SLICE;
-        if (rem == 5) dia_chunk<M, 1, XAOS, UNIFORM>(s, op, vp, xg, ldx, lbit, A, grow);
-        if (rem == 6) dia_chunk<M, 2, XAOS, UNIFORM>(s, op, vp, xg, ldx, lbit, A, grow);
-        if (rem == 7) dia_chunk<M, 3, XAOS, UNIFORM>(s, op, vp, xg, ldx, lbit, A, grow);
+        if (rem == 5) dia_chunk<M, 1, XAOS, UNIFORM, FULL>(s, op, vp, xg, ldx, lbit, A, grow);
+        if (rem == 6) dia_chunk<M, 2, XAOS, UNIFORM, FULL>(s, op, vp, xg, ldx, lbit, A, grow);
+        if (rem == 7) dia_chunk<M, 3, XAOS, UNIFORM, FULL>(s, op, vp, xg, ldx, lbit, A, grow);
     }
 }
 
@@ -281,11 +286,17 @@ __device__ __forceinline__ mw::V<mw::Arith<M>::W> spmv_row_dia(const SellMatrix 
     const double *__restrict__ xg = x + (A.row_base + row) * (XAOS ? W : 1);
     const ulonglong2 *__restrict__ op = A.pat + sw.w1;
     mw::V<W> s = mw::zero<W>();
+    // the predicate-free walk of full slices pays for FP64 only (C4 57.5 -> 51.1
+    // us/it); the multi-word modes lose more to the extra code than the selects
+    // cost (TW +12 %, QTW +5-9 %, DW/QDW +-2 %: profiles/r3d_full_slices_sweep.json)
+    const bool full = W == 1 && ((uint32_t)(d0 >> DIA_LBITS) & 0x200u) != 0;
     if (uniform) {
-        dia_walk<M, UU, XAOS, true>(s, L, op, nullptr, xg, ldx, lbit, A, A.row_base + row);
+        if (full) dia_walk<M, UU, XAOS, true, true>(s, L, op, nullptr, xg, ldx, lbit, A, A.row_base + row);
+        else dia_walk<M, UU, XAOS, true>(s, L, op, nullptr, xg, ldx, lbit, A, A.row_base + row);
     } else {
         const double *__restrict__ vp = A.vals + (((int64_t)(d0 & DIA_START_MASK) << 5) + ((int)row & 31));
-        dia_walk<M, U, XAOS, false>(s, L, op, vp, xg, ldx, lbit, A, A.row_base + row);
+        if (full) dia_walk<M, U, XAOS, false, true>(s, L, op, vp, xg, ldx, lbit, A, A.row_base + row);
+        else dia_walk<M, U, XAOS, false>(s, L, op, vp, xg, ldx, lbit, A, A.row_base + row);
     }
     return s;
 }

@@ -125,7 +125,8 @@ __global__ void sigma_slice_kernel(const I *__restrict__ rp, int64_t n_rows, con
 // per-lane values.
 // ---------------------------------------------------------------------------
 constexpr int DIA_SLACK = 2;
-constexpr int DIA_UNIFORM_BIT = 1 << 8;  // slice_info: slots | uniform << 8
+constexpr int DIA_UNIFORM_BIT = 1 << 8;  // slice_info: slots | uniform << 8 | full << 9
+constexpr int DIA_FULL_BIT = 1 << 9;     // every slot present in all 32 rows
 
 template <typename I, bool FILL>
 __global__ void dia_walk_kernel(const I *__restrict__ rp, const I *__restrict__ ci, const double *__restrict__ va,
@@ -149,6 +150,7 @@ __global__ void dia_walk_kernel(const I *__restrict__ rp, const I *__restrict__ 
     const int cap = min(len + DIA_SLACK, DIA_MAX_SLOTS);
     const int64_t g = row_base + r;
     bool uniform = FILL ? (slice_info[sl] & DIA_UNIFORM_BIT) != 0 : allow_uniform != 0;
+    bool full = true;
     const int64_t v0 = FILL ? val_ptr[sl] : 0;
     const int64_t r0 = FILL ? rec_ptr[sl] : 0;
     int k = 0;
@@ -166,6 +168,7 @@ __global__ void dia_walk_kernel(const I *__restrict__ rp, const I *__restrict__ 
         // value bits of the first present lane
         const unsigned long long first = __shfl_sync(0xffffffffu, bits, __ffs((int)mask) - 1);
         if (!FILL) uniform = uniform && __all_sync(0xffffffffu, !present || bits == first);
+        full = full && mask == 0xffffffffu;
         if (FILL) {
             if (lane == 0)
                 rec[r0 + k] = make_ulonglong2(((unsigned long long)mask << 32) | (unsigned long long)(uint32_t)m,
@@ -178,7 +181,7 @@ __global__ void dia_walk_kernel(const I *__restrict__ rp, const I *__restrict__ 
     if (!FILL && lane == 0) {
         val_sz[sl] = uniform ? 0 : (int64_t)k * SLICE;
         rec_sz[sl] = k;
-        slice_info[sl] = k | (uniform ? DIA_UNIFORM_BIT : 0);
+        slice_info[sl] = k | (uniform ? DIA_UNIFORM_BIT : 0) | (full && k > 0 ? DIA_FULL_BIT : 0);
     }
 }
 
@@ -242,7 +245,9 @@ static int dia_patterns(SellMatrixOwned *M, const int64_t *val_ptr, const int64_
             n_recent = std::min(n_recent + 1, RECENT);
         }
         const uint64_t uni = (info[j] & DIA_UNIFORM_BIT) ? 1ull : 0ull;
-        desc[2 * j] = (uint64_t)(vp[j] >> 5) | ((uint64_t)len << DIA_LBITS) | (uni << (DIA_LBITS + 8));
+        const uint64_t ful = (info[j] & DIA_FULL_BIT) ? 1ull : 0ull;
+        desc[2 * j] = (uint64_t)(vp[j] >> 5) | ((uint64_t)len << DIA_LBITS) | (uni << (DIA_LBITS + 8)) |
+                      (ful << (DIA_LBITS + 9));
         desc[2 * j + 1] = (uint64_t)base;
     }
     if (pat.empty()) pat.assign(DIA_PAD, make_ulonglong2(0ull, 0ull));
