@@ -1,5 +1,8 @@
 """Parity AT SCALE (north_star): full GPU solves of the
-BASELINE configs C2, C3, C4 and a C5-style instance in the fast tile order,
+BASELINE configs C2, C3, C4 (the modes whose hours-long host goldens exist), a
+C4-style instance at n = 1e5 (the C4 generator, every arithmetic: the
+ill-conditioned case where precision moves the iteration count) and a C5-style
+instance in the fast tile order,
 against the reference's own order run to convergence by the pinned oracle
 (cg_solve(..., partitions=1), the reference default: cg.py:42, sequential
 dot _fast.py:342-356, bounds kernels.py:158-162; goldens in
