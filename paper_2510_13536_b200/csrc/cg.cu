@@ -40,20 +40,42 @@ __device__ __forceinline__ void set_cond(cudaGraphConditionalHandle h, int use_c
 }
 
 // ---------------------------------------------------------------- scalar steps
+// The scalar inputs of a step (rho, k, the stop parameters) are loaded by the
+// last CTA's thread 0 BEFORE it joins the reduction of the partials, so their
+// L2 round trip runs under the reduction instead of after it (the serial
+// tail of K1 / K2 is pure latency: DESIGN.md §3).
+struct ScalarIn {
+    double rho[3];
+    long long k, k_stop, max_iters;
+    double b_norm, eps;
+};
+__device__ __forceinline__ ScalarIn scalar_inputs(const CgState *st) {
+    ScalarIn in;
+    for (int i = 0; i < 3; i++) in.rho[i] = st->rho[i];
+    in.k = st->k;
+    in.k_stop = st->k_stop;
+    in.max_iters = st->max_iters;
+    in.b_norm = st->b_norm;
+    in.eps = st->eps;
+    return in;
+}
+
 template <int M>
-__device__ void scalar_alpha(CgState *st, V<Arith<M>::W> pq, cudaGraphConditionalHandle h, int use_cond) {
+__device__ void scalar_alpha(CgState *st, V<Arith<M>::W> pq, cudaGraphConditionalHandle h, int use_cond,
+                             const ScalarIn *pre = nullptr) {
     using Ar = Arith<M>;
     constexpr int W = Ar::W;
+    ScalarIn in = pre ? *pre : scalar_inputs(st);
     for (int k = 0; k < W; k++) st->pq[k] = pq.w[k];
     double pq_f = Ar::collapse(pq);
     if (pq_f == 0.0 || !isfinite(pq_f)) {
         st->status = BREAKDOWN;
-        st->iterations = st->k;  // finish(False, "breakdown", k - 1): cg.py:157-158
+        st->iterations = in.k;  // finish(False, "breakdown", k - 1): cg.py:157-158
         set_cond(h, use_cond, 0u);
         return;
     }
     V<W> rho;
-    for (int k = 0; k < W; k++) rho.w[k] = st->rho[k];
+    for (int k = 0; k < W; k++) rho.w[k] = in.rho[k];
     V<W> a = Ar::div(rho, pq);
     for (int k = 0; k < W; k++) {
         st->alpha[k] = a.w[k];
@@ -63,17 +85,18 @@ __device__ void scalar_alpha(CgState *st, V<Arith<M>::W> pq, cudaGraphConditiona
 
 template <int M>
 __device__ void scalar_beta(CgState *st, V<Arith<M>::W> rho_new, cudaGraphConditionalHandle h,
-                            int use_cond) {
+                            int use_cond, const ScalarIn *pre = nullptr) {
     using Ar = Arith<M>;
     constexpr int W = Ar::W;
-    long long k = st->k + 1;
+    ScalarIn in = pre ? *pre : scalar_inputs(st);
+    long long k = in.k + 1;
     st->k = k;
     st->x_pending = 1;  // K3 applies x += alpha p (cg.py:162) for this iteration
     for (int i = 0; i < W; i++) st->rho_new[i] = rho_new.w[i];
     double rf = Ar::collapse(rho_new);
-    double rel = sqrt(fabs(rf)) / st->b_norm;  // rel_residual: cg.py:125-127
+    double rel = sqrt(fabs(rf)) / in.b_norm;  // rel_residual: cg.py:125-127
     st->rel = rel;
-    if (rel < st->eps) {
+    if (rel < in.eps) {
         st->status = CONVERGED;
         st->iterations = k;
     } else if (rf == 0.0 || !isfinite(rf)) {
@@ -81,18 +104,18 @@ __device__ void scalar_beta(CgState *st, V<Arith<M>::W> rho_new, cudaGraphCondit
         st->iterations = k;
     } else {
         V<W> rho;
-        for (int i = 0; i < W; i++) rho.w[i] = st->rho[i];
+        for (int i = 0; i < W; i++) rho.w[i] = in.rho[i];
         V<W> b = Ar::div(rho_new, rho);
         for (int i = 0; i < W; i++) {
             st->beta[i] = b.w[i];
             st->rho[i] = rho_new.w[i];
         }
-        if (k >= st->max_iters) {
+        if (k >= in.max_iters) {
             st->status = MAX_ITERS;
             st->iterations = k;
         }
     }
-    set_cond(h, use_cond, (st->status == RUNNING && k < st->k_stop) ? 1u : 0u);
+    set_cond(h, use_cond, (st->status == RUNNING && k < in.k_stop) ? 1u : 0u);
 }
 
 template <int M>
@@ -345,10 +368,12 @@ __global__ void __launch_bounds__(SpTraits<M>::THREADS, SpTraits<M>::MINB)
     }
     if (!FUSED || !g.final_ || (BLK && g.acc_out)) return;
     if (!last_block_done(&st->ticket[0], &s_last)) return;
+    ScalarIn in{};
+    if (threadIdx.x == 0) in = scalar_inputs(st);
     V<W> pq = reduce_partials_first<M>(part, g.part_ld, g.ntiles_glob, smem);
     if (threadIdx.x == 0) {
         st->ticket[0] = 0u;
-        scalar_alpha<M>(st, pq, h, use_cond);
+        scalar_alpha<M>(st, pq, h, use_cond, &in);
     }
 }
 
@@ -428,10 +453,12 @@ __global__ void __launch_bounds__(TILE_THREADS, Hoist<M>::MINB)
     }
     if (!FUSED || !g.final_) return;
     if (!last_block_done(&st->ticket[1], &s_last)) return;
+    ScalarIn in{};
+    if (threadIdx.x == 0) in = scalar_inputs(st);
     V<W> rn = reduce_partials_block<M>(part, g.part_ld, g.ntiles_glob, smem);
     if (threadIdx.x == 0) {
         st->ticket[1] = 0u;
-        scalar_beta<M>(st, rn, h, use_cond);
+        scalar_beta<M>(st, rn, h, use_cond, &in);
     }
 }
 
@@ -669,10 +696,12 @@ __global__ void __launch_bounds__(TILE_THREADS, UpTma<M>::MINB)
     }
     if (!FUSED || !g.final_) return;
     if (!last_block_done(&st->ticket[1], &s_last)) return;
+    ScalarIn in{};
+    if (threadIdx.x == 0) in = scalar_inputs(st);
     V<W> rn = reduce_partials_block<M>(part, g.part_ld, g.ntiles_glob, smem);
     if (threadIdx.x == 0) {
         st->ticket[1] = 0u;
-        scalar_beta<M>(st, rn, h, use_cond);
+        scalar_beta<M>(st, rn, h, use_cond, &in);
     }
 }
 
