@@ -116,8 +116,9 @@ int mwcg_matrix_create_ex(mwcg_matrix **out, int64_t n_rows, int64_t n_cols, int
                           int index_bytes, int64_t row_base, int col_format, void *stream);
 int mwcg_matrix_col_bytes(const mwcg_matrix *A);   /* 2 (int16 deltas), 4 (int32), 0 (slice-shared) */
 int mwcg_matrix_sigma_sorted(const mwcg_matrix *A); /* 1 if the rows of each tile are length-sorted */
-/* Column blocks: an irregular (int32-SELL) matrix with >= 2^22 columns also
- * keeps its entries cut into column ranges of 2^21 (MWCG_COLBLOCK=<columns>
+/* Column blocks: an irregular (int32-SELL) matrix with >= 2^22 columns, at
+ * least 10 % of whose entries lie 2^21 or more columns away from their row,
+ * also keeps its entries cut into column ranges of 2^21 (MWCG_COLBLOCK=<columns>
  * overrides, 0 = off); the solver's SpMV walks the ranges in turn, each
  * row's running sum carried in q, so one pass gathers only a range of p that
  * fits the L2.  Same additions in the same order: bitwise-identical q. */

@@ -1385,9 +1385,17 @@ int mwcg_matrix_create_blocked(mwcg_matrix **out, int64_t n_rows, int64_t n_cols
     // overrides (0: off); default 2^21 columns (a 32-MB range of a DW p) once
     // the matrix has at least twice as many.
     int64_t cpb = (n_cols >= ((int64_t)1 << 22)) ? ((int64_t)1 << 21) : 0;
-    if (const char *e = std::getenv("MWCG_COLBLOCK")) cpb = std::atoll(e);
-    if (cols_per_block >= 0) cpb = cols_per_block;  // the caller's choice (0: none)
-    rc = sell_colblocks(A->blocks, M, row_ptr, col_idx, values, index_bytes, cpb, (cudaStream_t)stream);
+    bool automatic = true;
+    if (const char *e = std::getenv("MWCG_COLBLOCK")) {
+        cpb = std::atoll(e);
+        automatic = false;
+    }
+    if (cols_per_block >= 0) {  // the caller's choice (0: none)
+        cpb = cols_per_block;
+        automatic = false;
+    }
+    rc = sell_colblocks(A->blocks, M, row_ptr, col_idx, values, index_bytes, cpb, automatic,
+                        (cudaStream_t)stream);
     if (rc) {
         sell_destroy(M);
         delete A;

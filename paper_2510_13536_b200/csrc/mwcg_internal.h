@@ -33,11 +33,12 @@ int sell_create(SellMatrixOwned **out, int64_t n_rows, int64_t n_cols, int64_t n
                 int64_t row_base, int col_format, cudaStream_t st);
 void sell_destroy(SellMatrixOwned *M);
 // Column blocks of an int32-SELL matrix (sell.cu): `out` stays empty when the
-// layout is banded (slice-shared / int16 deltas), cols_per_block <= 0, or
-// the matrix has at most cols_per_block columns.
+// layout is banded (slice-shared / int16 deltas), cols_per_block <= 0, the
+// matrix has at most cols_per_block columns, or (automatic) fewer than 10 % of
+// its entries lie cols_per_block or more columns away from their row.
 int sell_colblocks(std::vector<SellMatrixOwned *> &out, const SellMatrixOwned *M, const void *row_ptr,
                    const void *col_idx, const double *values, int index_bytes, int64_t cols_per_block,
-                   cudaStream_t st);
+                   bool automatic, cudaStream_t st);
 
 // operator-level launches (ops.cu); all stream-ordered
 int launch_spmv(int mode, const SellMatrix &A, const double *x, int64_t ldx, double *y, int64_t ldy,

@@ -568,6 +568,38 @@ __global__ void colblock_fill_kernel(const I *__restrict__ ci, const double *__r
     }
 }
 
+// entries whose column lies at least `width` away from their row: the gathers
+// that leave the row's L2-resident neighbourhood (what column blocks are for)
+template <typename I>
+__global__ void far_entries_kernel(const I *__restrict__ rp, const I *__restrict__ ci, int64_t n_rows,
+                                   int64_t row_base, int64_t width, unsigned long long *__restrict__ far) {
+    const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (r >= n_rows) return;
+    unsigned int c = 0;
+    for (int64_t k = rp[r] + lane; k < rp[r + 1]; k += 32) {
+        const int64_t d = (int64_t)ci[k] - (row_base + r);
+        c += (d >= width || d <= -width);
+    }
+    c = __reduce_add_sync(0xffffffffu, c);
+    if (lane == 0 && c) atomicAdd(far, (unsigned long long)c);
+}
+
+template <typename I>
+static int far_fraction(double *out, const SellMatrix &A, const I *rp, const I *ci, int64_t width,
+                        cudaStream_t st) {
+    unsigned long long *d = nullptr, h = 0;
+    MWCG_CUDA(pool_alloc((void **)&d, sizeof(unsigned long long), st));
+    MWCG_CUDA(cudaMemsetAsync(d, 0, sizeof(unsigned long long), st));
+    far_entries_kernel<I><<<(unsigned)((A.n_rows * 32 + 255) / 256), 256, 0, st>>>(rp, ci, A.n_rows, A.row_base,
+                                                                                  width, d);
+    MWCG_CUDA(cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, st));
+    MWCG_CUDA(cudaStreamSynchronize(st));
+    pool_free(d, st);
+    *out = A.nnz > 0 ? (double)h / (double)A.nnz : 0.0;
+    return 0;
+}
+
 template <typename I>
 static int build_colblocks(std::vector<SellMatrixOwned *> &out, const SellMatrix &full, const I *rp, const I *ci,
                            const double *va, int64_t cols_per_block, cudaStream_t st) {
@@ -629,10 +661,23 @@ static int build_colblocks(std::vector<SellMatrixOwned *> &out, const SellMatrix
 
 int sell_colblocks(std::vector<SellMatrixOwned *> &out, const SellMatrixOwned *M, const void *row_ptr,
                    const void *col_idx, const double *values, int index_bytes, int64_t cols_per_block,
-                   cudaStream_t st) {
+                   bool automatic, cudaStream_t st) {
     out.clear();
     const SellMatrix &A = M->view;
     if (cols_per_block <= 0 || A.dia || A.col16 || A.n_rows == 0 || A.n_cols <= cols_per_block) return 0;
+    if (automatic) {
+        // the automatic choice also asks that the far gathers matter: a matrix
+        // whose columns stay near the diagonal (irregular but local) gains
+        // nothing from the passes and would pay their per-row overhead
+        double far = 0.0;
+        const int rc = index_bytes == 8
+                           ? far_fraction<int64_t>(&far, A, (const int64_t *)row_ptr, (const int64_t *)col_idx,
+                                                   cols_per_block, st)
+                           : far_fraction<int32_t>(&far, A, (const int32_t *)row_ptr, (const int32_t *)col_idx,
+                                                   cols_per_block, st);
+        if (rc) return rc;
+        if (far < 0.10) return 0;
+    }
     return index_bytes == 8
                ? build_colblocks<int64_t>(out, A, (const int64_t *)row_ptr, (const int64_t *)col_idx, values,
                                           cols_per_block, st)

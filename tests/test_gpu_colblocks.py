@@ -160,3 +160,31 @@ def test_pipelined_exchange_with_several_blocks_per_slice(monkeypatch):
     res, x = solve_partitioned(_copy(A), b, 2, mode="dw", epsilon=1e-24, max_iterations=2000, pipeline=True)
     assert res.iterations == single.iterations
     assert np.array_equal(x.cpu().numpy().view(np.uint64), single.x.planes.cpu().numpy().view(np.uint64))
+
+
+def test_automatic_blocks_need_far_gathers():
+    """Automatic choice (no MWCG_COLBLOCK, >= 2^22 columns): blocks only when at
+    least 10 % of the entries lie 2^21 or more columns away from their row."""
+    n = (1 << 22) + 5000
+    rows = np.arange(n, dtype=np.int64)
+    rng = np.random.default_rng(8)
+
+    def build(far_cols, near=None):
+        if near is None:
+            near = np.clip(rows + rng.integers(33000, 50000, n), 0, n - 1)   # irregular, beyond int16 deltas
+        cols = np.stack([rows, near, far_cols], axis=1)
+        cols.sort(axis=1)
+        keep = np.ones_like(cols, dtype=bool)
+        keep[:, 1:] = cols[:, 1:] != cols[:, :-1]                        # drop duplicate columns
+        rp = np.zeros(n + 1, dtype=np.int64)
+        np.cumsum(keep.sum(axis=1), out=rp[1:])
+        return CsrMatrix(n, n, rp, cols[keep], np.ones(int(keep.sum())))
+
+    local = build(np.clip(rows - rng.integers(33000, 50000, n), 0, n - 1))
+    dm = K.device_matrix(local)
+    assert dm.col_bytes() == 4 and dm.col_blocks() == 0
+    local.release_device()
+    # two uniform columns per row: a quarter of them >= 2^21 away -> 1/6 of the entries
+    spread = build(rng.integers(0, n, n), rng.integers(0, n, n))
+    dm = K.device_matrix(spread)
+    assert dm.col_bytes() == 4 and dm.col_blocks() == 3 and dm.block_columns() == 1 << 21
