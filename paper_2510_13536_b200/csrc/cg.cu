@@ -21,6 +21,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdlib>
+#include <mutex>
 #include <vector>
 #include "ops.cuh"
 #include "tma.cuh"
@@ -1175,6 +1176,23 @@ int enqueue_dist_stage(mwcg_solver *s, int stage) {
     return 0;
 }
 
+// Process-wide persisting-L2 set-aside: set under a lock and only ever grown
+// (32 MB for 2-word, 40 MB for 3-word records), so solvers of different
+// arithmetics alternating in one process do not reconfigure the L2 on every
+// switch; each solver's window hit ratio follows the size actually in force.
+size_t configure_l2_aside(size_t aside) {
+    static std::mutex mu;
+    static size_t configured = 0;
+    std::lock_guard<std::mutex> lock(mu);
+    if (aside > configured) {
+        if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, aside) == cudaSuccess) configured = aside;
+    }
+    size_t cur = 0;
+    if (cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize) != cudaSuccess) cur = 0;
+    cudaGetLastError();  // both calls are advisory
+    return cur;
+}
+
 template <int M>
 int compute_grids_t(mwcg_solver *s) {
     int dev = 0, sms = 0;
@@ -1201,13 +1219,7 @@ int compute_grids_t(mwcg_solver *s) {
             // the device-wide set-aside is configured once per process and size
             // (re-setting it per solver reconfigures the L2: seen as a 2x slower
             // create-solve-destroy loop)
-            static size_t configured = 0;
-            if (configured != aside) {
-                cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, aside);
-                configured = aside;
-            }
-            size_t cur = 0;
-            cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+            const size_t cur = configure_l2_aside(aside);
             const size_t win = std::min(pbytes, (size_t)max_win);
             s->l2_aside = cur;
             s->l2win.base_ptr = s->p;
