@@ -590,7 +590,10 @@ struct UpTma {
 #ifdef MWCG_UP_TMA_MINB
     static constexpr int MINB = MWCG_UP_TMA_MINB;
 #else
-    static constexpr int MINB = 1;
+    // keeps the 2-word modes at 3 CTAs per SM (<= 85 registers) and the 3-word
+    // ones at 2: left to itself ptxas takes 94 registers for DW and drops a CTA
+    // (C3 / C4 DW +7-9 % per iteration)
+    static constexpr int MINB = (W <= 2) ? 3 : 2;
 #endif
 };
 template <int M>
